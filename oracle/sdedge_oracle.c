@@ -1,0 +1,363 @@
+/*
+ * sdedge_oracle.c -- TEST INFRASTRUCTURE ONLY (see sdedge_oracle.h).
+ *
+ * A plain, slow, literal fp64 implementation of the paper's solver:
+ *   P1 closed-form bandwidth, P2 Algorithm 1 with the
+ *   repairs listed in DESIGN.md ("Readings"), P3 enumeration of the
+ *   speculation length.
+ * Stage times are computed literally, pass by pass, from eq:flops_d /
+ * eq:flops_v / eq:latency_b2 / eq:d_latency / eq:v_latency for every
+ * candidate (i, j) and every decoding step n, exactly as Algorithm 1 lines
+ * 12-15 prescribe.  No closed forms, no blocking, no reordering.
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared -pthread (no -ffast-math).
+ */
+#include "sdedge_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* eq:ol: L = (1 - alpha^{1+l}) / (1 - alpha).
+ * Reading A2: alpha^{1+l} by repeated multiplication, each op rounded.   */
+double orc_expected_tokens(double alpha, int gamma)
+{
+    double A = alpha;
+    for (int t = 0; t < gamma; ++t) A = A * alpha;
+    return (1.0 - A) / (1.0 - alpha);
+}
+
+/* eq:step_n: n_m = ceil(O_m / L), with O_m = O_max. */
+int32_t orc_decode_steps(int32_t O, double L)
+{
+    double q = (double)O / L;
+    return (int32_t)ceil(q);
+}
+
+/* eq:memory_model: Gamma_p = J (8 h1^2 + 4 h1 h2) bytes (FP16). */
+int64_t orc_param_memory(int32_t J, int32_t h1, int32_t h2)
+{
+    return (int64_t)J * (8 * (int64_t)h1 * h1 + 4 * (int64_t)h1 * h2);
+}
+
+/* eq:memory_kv: per task 4 J h1 (I_m + O_m) bytes. */
+int64_t orc_kv_memory_per_task(int32_t J, int32_t h1, int32_t I, int32_t O)
+{
+    return 4 * (int64_t)J * h1 * ((int64_t)I + O);
+}
+
+/* eq:flops_d: FLOPs of the i-th draft forward pass at step n. */
+double orc_flops_draft(int32_t J, int32_t h1, int32_t h2, double Im, double L, int i, int n)
+{
+    if (n == 1 && i == 1)
+        return 4.0 * J * h1 * Im * (2.0 * h1 + Im + h2);
+    double Ikv = Im + ((n - 1) * L - 1.0) + i - 1; /* I^{kv,d}_{i,n,m} */
+    return 4.0 * J * h1 * (2.0 * h1 + Ikv + 1.0 + h2);
+}
+
+/* eq:flops_v: FLOPs of the verify pass at step n (l = gamma). */
+double orc_flops_verify(int32_t J, int32_t h1, int32_t h2, double Im, int gamma, double L, int n)
+{
+    if (n == 1)
+        return 4.0 * J * h1 * (Im + gamma) * (2.0 * h1 + Im + gamma + h2);
+    double Ikv = Im + (n - 1) * L - 1.0; /* I^{kv,v}_{n,m} */
+    return 4.0 * J * h1 * (1.0 + gamma) * (2.0 * h1 + Ikv + gamma + 1.0 + h2);
+}
+
+/* eq:latency_b2: T(b, F) = c1 F b + c2. */
+double orc_runtime(double c1, double c2, double F, double b)
+{
+    return c1 * F * b + c2;
+}
+
+static void coeffs_of(const orc_params* P, const double* co, double* c1d, double* c2d,
+                      double* c1v, double* c2v)
+{
+    if (co) { *c1d = co[0]; *c2d = co[1]; *c1v = co[2]; *c2v = co[3]; }
+    else    { *c1d = P->c1d; *c2d = P->c2d; *c1v = P->c1v; *c2v = P->c2v; }
+}
+
+/* eq:d_latency: T^d_{n,m} = sum_{i=1}^{l} (c1d F^d_{i,n,m} b + c2d). */
+double orc_draft_time(const orc_params* P, const double* co, int b, int32_t Im, int gamma,
+                      double L, int n)
+{
+    double c1d, c2d, c1v, c2v;
+    coeffs_of(P, co, &c1d, &c2d, &c1v, &c2v);
+    double t = 0.0;
+    for (int i = 1; i <= gamma; ++i)
+        t += orc_runtime(c1d, c2d, orc_flops_draft(P->Jd, P->h1d, P->h2d, (double)Im, L, i, n), (double)b);
+    return t;
+}
+
+/* eq:v_latency: T^v_{n,m} = c1v F^v_{n,m} b + c2v
+ * (+ optional downlink constant, reading A12; 0 by default). */
+double orc_verify_time(const orc_params* P, const double* co, int b, int32_t Im, int gamma,
+                       double L, int n)
+{
+    double c1d, c2d, c1v, c2v;
+    coeffs_of(P, co, &c1d, &c2d, &c1v, &c2v);
+    return orc_runtime(c1v, c2v, orc_flops_verify(P->Jv, P->h1v, P->h2v, (double)Im, gamma, L, n),
+                       (double)b) + P->downlink_s;
+}
+
+/* Memory feasibility of a batch of b tasks padded to Im (cons. (b) P:551,
+ * Alg. 1 lines 10-13).  128-bit so the literal product cannot overflow. */
+static int batch_fits(const orc_params* P, int b, int32_t Im)
+{
+    __int128 mem = (__int128)orc_param_memory(P->Jd, P->h1d, P->h2d)
+                 + (__int128)b * orc_kv_memory_per_task(P->Jd, P->h1d, Im, P->O_max);
+    return mem <= (__int128)P->gamma_s;
+}
+
+/* t*_com and eq:opt_w.  The printed t* has "p_k/g_k sigma^2"
+ * (P:608); reading A14 uses p_k g_k / sigma^2 as in eq:ul_latency_k. */
+double orc_bandwidth(const orc_params* P, const int32_t* I, const double* p, const double* g, double* w)
+{
+    const int K = P->K;
+    const double lam = P->lambda > 0 ? P->lambda : 16.0 * (P->h1d + P->h1v);
+    double tcom = 0.0, denom = 0.0;
+    for (int k = 0; k < K; ++k) {
+        double snr = p[k] * g[k] / P->sigma2;
+        double s = log2(1.0 + snr);
+        tcom += lam * I[k] / (P->Bw * s);
+        denom += I[k] / s;
+    }
+    if (w)
+        for (int k = 0; k < K; ++k) {
+            double snr = p[k] * g[k] / P->sigma2;
+            double s = log2(1.0 + snr);
+            w[k] = (I[k] / s) / denom;
+        }
+    return tcom;
+}
+
+/* eq:time, eq:latency_infer_batch, eq:latency_inf for a given
+ * plan under uniform O_max planning (M_n = M). */
+double orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                     int gamma, int M, const int32_t* batch_end)
+{
+    double L = orc_expected_tokens(alpha, gamma);
+    int N = orc_decode_steps(P->O_max, L);
+    for (int m = 0; m < M; ++m) {
+        int start = m ? batch_end[m - 1] + 1 : 1;
+        if (!batch_fits(P, batch_end[m] - start + 1, Is[batch_end[m] - 1])) return INFINITY;
+    }
+    double Tinf = 0.0;
+    for (int n = 1; n <= N; ++n) {
+        double Cd = 0.0, C = 0.0; /* C_{n,0} = 0 */
+        for (int m = 0; m < M; ++m) {
+            int start = m ? batch_end[m - 1] + 1 : 1;
+            int b = batch_end[m] - start + 1;
+            int32_t Im = Is[batch_end[m] - 1]; /* sorted: max is the last */
+            Cd += orc_draft_time(P, co, b, Im, gamma, L, n);         /* C^d_{n,m} */
+            double st = Cd > C ? Cd : C;                             /* max{C^d, C_{n,m-1}} */
+            C = st + orc_verify_time(P, co, b, Im, gamma, L, n);     /* eq:time */
+        }
+        Tinf += C; /* T_n = C_{n,M} */
+    }
+    return Tinf;
+}
+
+/* Algorithm 1 with readings A1 (bracket of eq:t_ij1), A3 (K+1
+ * rows, row 0 = 0, best = +inf), A4 (S[i] always set), A6 (largest j wins
+ * ties: the ">=" of line 21). */
+double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+              int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j)
+{
+    const int K = P->K;
+    double L = orc_expected_tokens(alpha, gamma);
+    int N = orc_decode_steps(P->O_max, L);
+    size_t rowlen = (size_t)(N + 1) * 2;
+    double* Y = (double*)calloc((size_t)(K + 1) * rowlen, sizeof(double)); /* Upsilon */
+    double* Td = (double*)malloc((size_t)(N + 1) * sizeof(double));
+    double* Tv = (double*)malloc((size_t)(N + 1) * sizeof(double));
+#define UPS(i, n, s) Y[(size_t)(i) * rowlen + (size_t)(n) * 2 + (s)]
+    double result = 0.0;
+    for (int i = 1; i <= K; ++i) {
+        double best = INFINITY, second = INFINITY;
+        int jstar = 0;
+        int32_t Im = Is[i - 1]; /* max input length of tasks j..i */
+        for (int j = 1; j <= i; ++j) {
+            if (i == force_row && j != force_j) continue;
+            int b = i - j + 1;
+            if (!batch_fits(P, b, Im)) continue; /* Alg. 1 lines 10-13 */
+            for (int n = 1; n <= N; ++n) {      /* Alg. 1 lines 14-15 */
+                Tv[n] = orc_verify_time(P, co, b, Im, gamma, L, n);
+                Td[n] = orc_draft_time(P, co, b, Im, gamma, L, n);
+            }
+            double temp = 0.0;                  /* Alg. 1 line 15, eq:t_ij1 (A1) */
+            for (int n = 1; n <= N; ++n) {
+                double d0 = UPS(j - 1, n, 0) + Td[n];
+                double y1 = UPS(j - 1, n, 1);
+                temp += (d0 > y1 ? d0 : y1) + Tv[n];
+            }
+            if (W) *W += N;
+            if (best >= temp) { second = best; best = temp; jstar = j; } /* line 21 */
+            else if (temp < second) second = temp;
+        }
+        if (jstar == 0) { result = INFINITY; if (S) S[i - 1] = 0; break; } /* no feasible batch */
+        UPS(i, 0, 0) = best;                    /* eq:rg */
+        if (S) S[i - 1] = jstar;
+        if (row_gap) /* relative gap; an exact tie is a zero gap even at best == 0 */
+            row_gap[i - 1] = isinf(second) ? INFINITY : second == best ? 0.0 : (second - best) / fabs(best);
+        int b = i - jstar + 1;
+        for (int n = 1; n <= N; ++n) {          /* eq:tt1, eq:tt2 (line 26) */
+            double td = orc_draft_time(P, co, b, Im, gamma, L, n);
+            double tv = orc_verify_time(P, co, b, Im, gamma, L, n);
+            double d0 = UPS(jstar - 1, n, 0) + td;
+            double y1 = UPS(jstar - 1, n, 1);
+            UPS(i, n, 0) = d0;
+            UPS(i, n, 1) = (d0 > y1 ? d0 : y1) + tv;
+        }
+        result = best;
+    }
+#undef UPS
+    free(Y); free(Td); free(Tv);
+    return result;
+}
+
+/* Stable ascending sort of task indices by I_k (reading A13). */
+static void sort_tasks(int K, const int32_t* I, int32_t* order)
+{
+    for (int k = 0; k < K; ++k) order[k] = k;
+    for (int a = 1; a < K; ++a) { /* insertion sort: stable */
+        int32_t t = order[a];
+        int c = a - 1;
+        while (c >= 0 && I[order[c]] > I[t]) { order[c + 1] = order[c]; --c; }
+        order[c + 1] = t;
+    }
+}
+
+void orc_solve(const orc_params* P, const int32_t* I, const double* p, const double* g,
+               double alpha, const double* coeffs4, orc_result* R, int32_t* order,
+               int32_t* batch_end, double* w, double* tinf_gamma)
+{
+    const int K = P->K;
+    const int ng = P->gamma_max - P->gamma_min + 1;
+    memset(R, 0, sizeof(*R));
+    R->gamma = -1; R->min_row_gap = INFINITY; R->gamma_gap = INFINITY;
+    R->gap_gamma = -1; R->gap_row = -1;
+    for (int k = 0; k < K; ++k) batch_end[k] = 0;
+    sort_tasks(K, I, order);
+
+    int bad_task = 0;
+    for (int k = 0; k < K; ++k)
+        if (I[k] < 1 || !(p[k] > 0) || !(g[k] > 0) || !isfinite(p[k]) || !isfinite(g[k])) bad_task = 1;
+    if (bad_task) {
+        R->status = 3;
+        R->T = R->T_com = R->T_inf = NAN;
+        for (int k = 0; k < K; ++k) w[k] = NAN;
+        for (int q = 0; q < ng; ++q) tinf_gamma[q] = NAN;
+        return;
+    }
+    R->T_com = orc_bandwidth(P, I, p, g, w);
+    if (!(alpha > 0.0 && alpha < 1.0)) {
+        R->status = 2;
+        R->T = R->T_inf = NAN;
+        for (int q = 0; q < ng; ++q) tinf_gamma[q] = NAN;
+        return;
+    }
+    int32_t* Is = (int32_t*)malloc(sizeof(int32_t) * K);
+    int32_t* S = (int32_t*)malloc(sizeof(int32_t) * K);
+    int32_t* Sbest = (int32_t*)malloc(sizeof(int32_t) * K);
+    double* gap = (double*)malloc(sizeof(double) * K);
+    for (int k = 0; k < K; ++k) Is[k] = I[order[k]];
+
+    double best = INFINITY, second = INFINITY;
+    int gbest = -1;
+    for (int gm = P->gamma_min; gm <= P->gamma_max; ++gm) { /* P3 */
+        double t = orc_dp(P, coeffs4, Is, alpha, gm, S, gap, &R->W, 0, 0);
+        tinf_gamma[gm - P->gamma_min] = t;
+        if (isinf(t)) continue;
+        for (int r = 0; r < K; ++r)
+            if (gap[r] < R->min_row_gap) { R->min_row_gap = gap[r]; R->gap_gamma = gm; R->gap_row = r + 1; }
+        if (t < best) { second = best; best = t; gbest = gm; memcpy(Sbest, S, sizeof(int32_t) * K); }
+        else if (t < second) second = t; /* smallest gamma wins ties (reading A7) */
+    }
+    if (gbest < 0) {
+        R->status = 1;
+        R->T = R->T_inf = INFINITY;
+    } else {
+        R->gamma = gbest;
+        R->T_inf = best;
+        R->T = R->T_com + R->T_inf;
+        R->gamma_gap = isinf(second) ? INFINITY : (second - best) / best;
+        /* backtracking (reading A5: i <- S[i] - 1) */
+        int tmp[1024 + 1];
+        int M = 0, i = K;
+        while (i > 0) { tmp[M++] = i; i = Sbest[i - 1] - 1; }
+        for (int m = 0; m < M; ++m) batch_end[m] = tmp[M - 1 - m];
+        R->M = M;
+    }
+    free(Is); free(S); free(Sbest); free(gap);
+}
+
+double orc_brute_force(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                       int gamma_min, int gamma_max, int32_t* best_gamma, int32_t* best_M,
+                       int32_t* best_end)
+{
+    const int K = P->K;
+    double best = INFINITY;
+    int32_t ends[32];
+    *best_gamma = -1; *best_M = 0;
+    if (K > 20) return NAN;
+    for (int gm = gamma_min; gm <= gamma_max; ++gm) {
+        for (long mask = 0; mask < (1L << (K - 1)); ++mask) {
+            int M = 0;
+            for (int t = 0; t < K - 1; ++t)
+                if (mask & (1L << t)) ends[M++] = t + 1;
+            ends[M++] = K;
+            double v = orc_eval_plan(P, co, Is, alpha, gm, M, ends);
+            if (v < best) {
+                best = v; *best_gamma = gm; *best_M = M;
+                memcpy(best_end, ends, sizeof(int32_t) * M);
+            }
+        }
+    }
+    return best;
+}
+
+/* ---------------------------------------------------------------- batch */
+typedef struct {
+    const orc_params* P; int64_t n; const int32_t* I; const double *p, *g, *alpha, *coeffs;
+    int32_t *status, *gamma, *M; double* lat; int32_t *order, *batch_end; double* w;
+    double *min_row_gap, *gamma_gap; int64_t* W; int64_t next;
+} batch_ctx;
+
+static void* batch_worker(void* arg)
+{
+    batch_ctx* c = (batch_ctx*)arg;
+    const int K = c->P->K;
+    double* tg = (double*)malloc(sizeof(double) * (c->P->gamma_max - c->P->gamma_min + 1));
+    for (;;) {
+        int64_t s = __atomic_fetch_add(&c->next, 1, __ATOMIC_RELAXED);
+        if (s >= c->n) break;
+        orc_result R;
+        orc_solve(c->P, c->I + s * K, c->p + s * K, c->g + s * K, c->alpha[s],
+                  c->coeffs ? c->coeffs + s * 4 : NULL, &R, c->order + s * K,
+                  c->batch_end + s * K, c->w + s * K, tg);
+        c->status[s] = R.status; c->gamma[s] = R.gamma; c->M[s] = R.M;
+        c->lat[3 * s] = R.T; c->lat[3 * s + 1] = R.T_com; c->lat[3 * s + 2] = R.T_inf;
+        if (c->min_row_gap) c->min_row_gap[s] = R.min_row_gap;
+        if (c->gamma_gap) c->gamma_gap[s] = R.gamma_gap;
+        if (c->W) c->W[s] = R.W;
+    }
+    free(tg);
+    return NULL;
+}
+
+void orc_solve_batch(const orc_params* P, int64_t n, const int32_t* I, const double* p,
+                     const double* g, const double* alpha, const double* coeffs,
+                     int32_t* status, int32_t* gamma, int32_t* M, double* lat,
+                     int32_t* order, int32_t* batch_end, double* w, double* min_row_gap,
+                     double* gamma_gap, int64_t* W, int nthreads)
+{
+    batch_ctx c = {P, n, I, p, g, alpha, coeffs, status, gamma, M, lat, order, batch_end, w,
+                   min_row_gap, gamma_gap, W, 0};
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, batch_worker, &c);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}

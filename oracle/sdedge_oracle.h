@@ -1,0 +1,98 @@
+/*
+ * sdedge_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, literal CPU oracle for the joint bandwidth / batching /
+ * speculation-length solver of arXiv 2510.11331 ("Efficient LLM Inference
+ * over Heterogeneous Edge Networks with Speculative Decoding").
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header,
+ * table or constant with the CUDA path (paper_2510_11331_b200/).
+ *
+ * Citations: P:n = PAPER.md line n.  All arithmetic is IEEE fp64, built with
+ * -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ *
+ * Parity status of each function: see DESIGN.md section "Oracle pins".
+ * Every function is pinned (no "parity unpinned" entries).
+ */
+#ifndef SDEDGE_ORACLE_H
+#define SDEDGE_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    int32_t Jd, h1d, h2d;        /* draft model (Table I)             */
+    int32_t Jv, h1v, h2v;        /* verify model                                 */
+    double  c1d, c2d, c1v, c2v;  /* eq:latency_b2 coefficients (Table II)        */
+    double  Bw;                  /* uplink bandwidth B_w, Hz                     */
+    double  sigma2;              /* noise power, W                               */
+    double  lambda;              /* bits per token; <= 0 -> 16(h1d+h1v)  */
+    int64_t gamma_s;             /* SBS memory capacity Gamma_s, bytes           */
+    int32_t K, O_max, gamma_min, gamma_max;
+    double  downlink_s;          /* optional per-step, per-batch verify add-on   */
+} orc_params;
+
+typedef struct {
+    int32_t status;              /* 0 ok, 1 memory-infeasible, 2 bad alpha, 3 bad task */
+    int32_t gamma;               /* gamma*, -1 if status != 0                    */
+    int32_t M;                   /* number of batches                            */
+    double  T, T_com, T_inf;
+    double  min_row_gap;         /* min over gamma and rows of (2nd-best - best)/best */
+    int32_t gap_gamma, gap_row;  /* where min_row_gap occurred                   */
+    double  gamma_gap;           /* (2nd-best gamma T_inf - best)/best            */
+    int64_t W;                   /* candidate-steps evaluated                    */
+} orc_result;
+
+/* ---- paper primitives (each pinned in tests/test_oracle_pins.py) ---- */
+double  orc_expected_tokens(double alpha, int gamma);                 /* eq:ol      */
+int32_t orc_decode_steps(int32_t O, double L);                        /* eq:step_n  */
+int64_t orc_param_memory(int32_t J, int32_t h1, int32_t h2);          /* eq:memory_model */
+int64_t orc_kv_memory_per_task(int32_t J, int32_t h1, int32_t I, int32_t O); /* eq:memory_kv */
+double  orc_flops_draft(int32_t J, int32_t h1, int32_t h2, double Im, double L, int i, int n);  /* eq:flops_d */
+double  orc_flops_verify(int32_t J, int32_t h1, int32_t h2, double Im, int gamma, double L, int n); /* eq:flops_v */
+double  orc_runtime(double c1, double c2, double F, double b);        /* eq:latency_b2 */
+double  orc_draft_time(const orc_params* P, const double* co, int b, int32_t Im, int gamma, double L, int n); /* eq:d_latency */
+double  orc_verify_time(const orc_params* P, const double* co, int b, int32_t Im, int gamma, double L, int n); /* eq:v_latency */
+
+/* eq:opt_w / t*_com. Writes w[K]; returns t*_com. */
+double  orc_bandwidth(const orc_params* P, const int32_t* I, const double* p, const double* g, double* w);
+
+/* eq:time / eq:latency_inf: literal pipeline recursion of one plan.
+ * batches are given as sorted-position ends (1-based, ascending, last == K).
+ * Returns T_inf (planned, uniform O_max), +inf if a batch is memory-infeasible. */
+double  orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                      int gamma, int M, const int32_t* batch_end);
+
+/* Algorithm 1 for one gamma over sorted lengths Is[0..K-1].
+ * S[K] receives 1-based boundaries; returns Upsilon[K,0,0] (+inf if infeasible).
+ * row_gap[K] (optional) receives per-row relative gaps (+inf if < 2 candidates).
+ * force_row/force_j (optional, force_row < 1 disables) forces the choice j at
+ * one row -- used by the near-tie branching replay. */
+double  orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+               int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j);
+
+/* Full solve of problem P for one scenario.
+ * order[K], batch_end[K], w[K], tinf_gamma[gamma_max-gamma_min+1] are caller-owned. */
+void    orc_solve(const orc_params* P, const int32_t* I, const double* p, const double* g,
+                  double alpha, const double* coeffs4, orc_result* R, int32_t* order,
+                  int32_t* batch_end, double* w, double* tinf_gamma);
+
+/* Exhaustive search over every contiguous partition of the sorted order and
+ * every gamma (K <= 20).  Returns best T_inf; writes its plan. */
+double  orc_brute_force(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                        int gamma_min, int gamma_max, int32_t* best_gamma, int32_t* best_M,
+                        int32_t* best_end);
+
+/* Batch driver: n scenarios (SoA, row-major [n][K]) on nthreads pthreads. */
+void    orc_solve_batch(const orc_params* P, int64_t n, const int32_t* I, const double* p,
+                        const double* g, const double* alpha, const double* coeffs,
+                        int32_t* status, int32_t* gamma, int32_t* M, double* lat /*[n*3]*/,
+                        int32_t* order, int32_t* batch_end, double* w, double* min_row_gap,
+                        double* gamma_gap, int64_t* W, int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
