@@ -1,0 +1,134 @@
+/*
+ * sdedge.h -- C ABI of the B200-native batched solver for the joint
+ * bandwidth / batching / speculation-length problem of arXiv 2510.11331,
+ * "Efficient LLM Inference over Heterogeneous Edge Networks with Speculative
+ * Decoding".  Citations: P:n = PAPER.md line n.
+ *
+ * What one call computes, for each of n independent scenarios (problem P,
+ * P:543-566):
+ *   1. the closed-form optimal uplink bandwidth split w*_k and t*_com
+ *      (eq:bandw1 / eq:opt_w);
+ *   2. for every speculation length gamma in [gamma_min, gamma_max]
+ *      (P3): L = (1-alpha^{gamma+1})/(1-alpha) (eq:ol),
+ *      N = ceil(O_max / L) (eq:step_n, uniform O_max planning
+ *      P:638-641), and Algorithm 1 over the tasks sorted by input
+ *      length, with the candidate cost eq:t_ij1 / state update eq:tt1-tt2
+ *      evaluated under the latency model eq:flops_d, eq:flops_v,
+ *      eq:latency_b2, eq:d_latency, eq:v_latency, eq:time and the
+ *      memory constraint eq:memory_model + eq:memory_kv;
+ *   3. gamma* = the smallest gamma minimising T_inf, its batches recovered by
+ *      backtracking S, and T = T_com + T_inf.
+ * DESIGN.md "Readings" lists how the garbled / ambiguous passages are read
+ * (bracket of eq:t_ij1, Upsilon init, S[i] at j*=1, backtrack step, ties).
+ *
+ * Conventions
+ *   - Every array pointer in sdedge_scenarios / sdedge_schedule / out_latency
+ *     is a DEVICE pointer (cudaMalloc / torch CUDA tensor) on the current
+ *     device, row-major [scenario][task].  The caller owns all of them.
+ *     sdedge_solve_batch_host() is the same call on HOST pointers (pinned
+ *     memory recommended); it stages the copies itself.
+ *   - The call is asynchronous on params->stream (NULL = legacy default
+ *     stream); results are valid once that stream completes.  Workspace is
+ *     stream-ordered (cudaMallocAsync) and freed on the same stream.
+ *   - Per-scenario problems never fail the call: they set status[s] and
+ *     write gamma = -1, num_batches = 0, batch_end = 0 and
+ *       status 1 (memory-infeasible: some task fits in no batch, cons. (b)
+ *                 P:551):  out_latency = {+inf, T_com, +inf};
+ *       status 2 (alpha not in (0,1)):              {NaN, T_com, NaN};
+ *       status 3 (some I_k < 1, p_k or g_k not > 0 / not finite):
+ *                 {NaN, NaN, NaN}, bw_share = NaN.
+ *     order[] is always the stable sort; bw_share is valid for status 0-2.
+ *   - Return: 0 = enqueued; -1 = invalid argument (see sdedge_last_error());
+ *     -2 = CUDA error; -3 = out of device memory.
+ *   - Thread-safe and re-entrant across streams and devices (no global
+ *     mutable state besides the thread-local error string).
+ */
+#ifndef SDEDGE_H
+#define SDEDGE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDEDGE_ABI_VERSION 1
+#define SDEDGE_MAX_K 1024
+
+typedef struct {
+    int32_t layers;  /* J   (Table I)  >= 1 */
+    int32_t hidden;  /* h1  >= 1                        */
+    int32_t ffn;     /* h2  >= 1                        */
+} sdedge_model;
+
+typedef enum {
+    SDEDGE_ALGO_ENVELOPE = 0, /* closed-form sum over the piecewise-linear Upsilon envelope
+                                 (exact reformulation of eq:t_ij1, O(K^2 * segments))   */
+    SDEDGE_ALGO_DENSE = 1     /* eq:t_ij1 summed step by step over n = 1..N (O(K^2 N))   */
+} sdedge_algo;
+
+#define SDEDGE_FLAG_TINY_POOL 1
+
+typedef struct {
+    sdedge_model draft, verify;  /* SBS draft / MBS verify models                    */
+    double  c1_draft, c2_draft;  /* eq:latency_b2 coefficients of the SBS GPU, c1 > 0, c2 >= 0 */
+    double  c1_verify, c2_verify;/* ... of the MBS GPU (Table II: 4.11e-13, 0.56e-3, 2.08e-14, 1.28e-2) */
+    double  bandwidth_hz;        /* B_w > 0 (Table II: 20 MHz)                               */
+    double  noise_w;             /* sigma^2 > 0, linear watts (-106 dBm = 2.5118864315095823e-14) */
+    double  lambda_bits;         /* lambda, bits per input token; <= 0 -> 16 (h1d + h1v) */
+    int64_t mem_capacity_bytes;  /* Gamma_s of the SBS (Table II "16 GB" = 16e9)             */
+    int32_t K;                   /* tasks per scenario, 1..SDEDGE_MAX_K, same for all n      */
+    int32_t O_max;               /* planning output length, 1..2^20 (Table II: 2048)         */
+    int32_t gamma_min, gamma_max;/* 0 <= gamma_min <= gamma_max <= 64 (P:555 uses >= 1;
+                                    gamma = 0 is the autoregressive reduction)               */
+    int32_t precision;           /* 0 = fp64 DP arithmetic, 1 = fp32 variant                 */
+    int32_t algo;                /* sdedge_algo                                              */
+    int32_t flags;               /* 0, or SDEDGE_FLAG_TINY_POOL (test hook: an 8-segment first-pass
+                                    envelope pool, forcing the worst-case second pass)       */
+    double  downlink_s;          /* >= 0, added to every verify stage (P:424-427 says 0)     */
+    void*   stream;              /* cudaStream_t                                              */
+} sdedge_params;
+
+typedef struct {
+    const int32_t* input_len;    /* [n*K] I_k (tokens)                                      */
+    const double*  tx_power_w;   /* [n*K] p_k (W)                                           */
+    const double*  gain;         /* [n*K] g_k (linear)                                      */
+    const double*  alpha;        /* [n]   token acceptance rate                             */
+    const double*  coeffs;       /* [n*4] per-scenario (c1d, c2d, c1v, c2v) or NULL -> params */
+} sdedge_scenarios;
+
+typedef struct {
+    int32_t* gamma;              /* [n]   gamma* or -1                                       */
+    int32_t* num_batches;        /* [n]   M                                                 */
+    int32_t* batch_end;          /* [n*K] 1-based sorted position ending batch m (m < M), rest 0 */
+    int32_t* order;              /* [n*K] original task index at each sorted position        */
+    double*  bw_share;           /* [n*K] w*_k in ORIGINAL task order, or NULL               */
+    int32_t* status;             /* [n]                                                      */
+} sdedge_schedule;
+
+/* Solve n scenarios.  out_latency: [n*3] = {T, T_com, T_inf} (seconds). */
+int sdedge_solve_batch(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
+                       double* out_latency, sdedge_schedule* out_schedule);
+
+/* Same, HOST pointers for every array; copies in, solves and copies out on
+ * params->stream.  The caller synchronises the stream before reading. */
+int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
+                            double* out_latency, sdedge_schedule* out_schedule);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int sdedge_last_launch_count(void);
+
+/* Message for the last nonzero return on this thread ("" if none). */
+const char* sdedge_last_error(void);
+
+int sdedge_abi_version(void);
+
+/* FP64 / FP32 pipe peak microbenchmark (the roofline denominator):
+ * runs a DFMA (fp32: FFMA) chain on every SM of the current device and
+ * returns achieved FMA-lane operations per second in *ops_per_s (an FMA
+ * counts as one operation).  Synchronous.  Returns 0 or a negative error. */
+int sdedge_pipe_peak(int32_t fp32, double* ops_per_s, double* elapsed_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

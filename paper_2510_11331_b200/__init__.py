@@ -1,0 +1,179 @@
+"""Thin Python binding of the sm_100a solver library (include/sdedge.h).
+
+Argument marshalling only: every step of the solve runs inside
+libsdedge.so's CUDA kernels.  PyTorch provides device memory and streams.
+There is no CPU fallback: if the library is missing, import-time loading
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from ._build import LIB, build  # noqa: F401
+
+__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_pipe_peak", "sdedge_last_error",
+           "sdedge_last_launch_count", "sdedge_abi_version", "solve", "solve_host", "make_params",
+           "ALGO_ENVELOPE", "ALGO_DENSE", "EXPORTED_SYMBOLS", "lib"]
+
+ALGO_ENVELOPE, ALGO_DENSE = 0, 1
+FLAG_TINY_POOL = 1
+EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_last_launch_count",
+                    "sdedge_last_error", "sdedge_abi_version", "sdedge_pipe_peak")
+
+
+class SdedgeModel(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32)]
+
+
+class SdedgeParams(C.Structure):
+    _fields_ = [("draft", SdedgeModel), ("verify", SdedgeModel),
+                ("c1_draft", C.c_double), ("c2_draft", C.c_double),
+                ("c1_verify", C.c_double), ("c2_verify", C.c_double),
+                ("bandwidth_hz", C.c_double), ("noise_w", C.c_double), ("lambda_bits", C.c_double),
+                ("mem_capacity_bytes", C.c_int64), ("K", C.c_int32), ("O_max", C.c_int32),
+                ("gamma_min", C.c_int32), ("gamma_max", C.c_int32), ("precision", C.c_int32),
+                ("algo", C.c_int32), ("flags", C.c_int32), ("downlink_s", C.c_double),
+                ("stream", C.c_void_p)]
+
+
+class SdedgeScenarios(C.Structure):
+    _fields_ = [("input_len", C.c_void_p), ("tx_power_w", C.c_void_p), ("gain", C.c_void_p),
+                ("alpha", C.c_void_p), ("coeffs", C.c_void_p)]
+
+
+class SdedgeSchedule(C.Structure):
+    _fields_ = [("gamma", C.c_void_p), ("num_batches", C.c_void_p), ("batch_end", C.c_void_p),
+                ("order", C.c_void_p), ("bw_share", C.c_void_p), ("status", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libsdedge.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"{LIB} is missing: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB)
+        for f in ("sdedge_solve_batch", "sdedge_solve_batch_host"):
+            fn = getattr(L, f)
+            fn.restype = C.c_int
+            fn.argtypes = [C.POINTER(SdedgeScenarios), C.c_int64, C.POINTER(SdedgeParams), C.c_void_p,
+                           C.POINTER(SdedgeSchedule)]
+        L.sdedge_last_error.restype = C.c_char_p
+        L.sdedge_last_launch_count.restype = C.c_int
+        L.sdedge_abi_version.restype = C.c_int
+        L.sdedge_pipe_peak.restype = C.c_int
+        L.sdedge_pipe_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _lib = L
+    return _lib
+
+
+def sdedge_last_error() -> str:
+    return lib().sdedge_last_error().decode()
+
+
+def sdedge_last_launch_count() -> int:
+    return lib().sdedge_last_launch_count()
+
+
+def sdedge_abi_version() -> int:
+    return lib().sdedge_abi_version()
+
+
+def make_params(d: dict, stream=None, precision: int | None = None, algo: int | None = None) -> SdedgeParams:
+    """Marshal a parameter dict (scengen.params() layout) into sdedge_params."""
+    st = 0
+    if stream is not None:
+        st = stream if isinstance(stream, int) else int(stream.cuda_stream)
+    return SdedgeParams(SdedgeModel(*d["draft"]), SdedgeModel(*d["verify"]),
+                        d["c1_draft"], d["c2_draft"], d["c1_verify"], d["c2_verify"],
+                        d["bandwidth_hz"], d["noise_w"], d.get("lambda_bits", 0.0),
+                        int(d["mem_capacity_bytes"]), d["K"], d["O_max"], d["gamma_min"], d["gamma_max"],
+                        d.get("precision", 0) if precision is None else precision,
+                        d.get("algo", ALGO_ENVELOPE) if algo is None else algo, d.get("flags", 0),
+                        d.get("downlink_s", 0.0), st)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data  # numpy (host entry point)
+
+
+def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, status):
+    sc = SdedgeScenarios(_ptr(I), _ptr(p), _ptr(g), _ptr(alpha), _ptr(coeffs))
+    sch = SdedgeSchedule(_ptr(gamma), _ptr(M), _ptr(bend), _ptr(order), _ptr(w), _ptr(status))
+    rc = fn(C.byref(sc), n, C.byref(P), _ptr(lat), C.byref(sch))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_solve_batch failed ({rc}): {sdedge_last_error()}")
+    return rc
+
+
+def sdedge_solve_batch(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma, num_batches,
+                       batch_end, order, bw_share, status):
+    """Direct C-ABI call on DEVICE tensors (all contiguous, see include/sdedge.h)."""
+    return _call(lib().sdedge_solve_batch, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
+                 num_batches, batch_end, order, bw_share, status)
+
+
+def sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma,
+                            num_batches, batch_end, order, bw_share, status):
+    """Direct C-ABI call on HOST buffers (numpy or pinned torch CPU tensors)."""
+    return _call(lib().sdedge_solve_batch_host, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
+                 num_batches, batch_end, order, bw_share, status)
+
+
+def sdedge_pipe_peak(fp32: bool = False):
+    ops, el = C.c_double(0), C.c_double(0)
+    rc = lib().sdedge_pipe_peak(1 if fp32 else 0, C.byref(ops), C.byref(el))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_pipe_peak failed ({rc}): {sdedge_last_error()}")
+    return ops.value, el.value
+
+
+def _alloc_out(torch, n, K, device, want_w, pin=False):
+    kw = dict(device=device) if device is not None else dict(pin_memory=pin)
+    return dict(lat=torch.empty((n, 3), dtype=torch.float64, **kw),
+                gamma=torch.empty(n, dtype=torch.int32, **kw),
+                M=torch.empty(n, dtype=torch.int32, **kw),
+                batch_end=torch.empty((n, K), dtype=torch.int32, **kw),
+                order=torch.empty((n, K), dtype=torch.int32, **kw),
+                w=torch.empty((n, K), dtype=torch.float64, **kw) if want_w else None,
+                status=torch.empty(n, dtype=torch.int32, **kw))
+
+
+def solve(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream=None, out=None,
+          precision: int | None = None, algo: int | None = None) -> dict:
+    """Solve scenarios held in CUDA tensors; returns CUDA output tensors
+    (enqueued on `stream`, default torch's current stream)."""
+    import torch
+    n, K = I.shape
+    dev = I.device
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)
+    o = out if out is not None else _alloc_out(torch, n, K, dev, want_w)
+    sdedge_solve_batch(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end"],
+                       o["order"], o["w"], o["status"])
+    return o
+
+
+def solve_host(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream=None, out=None,
+               precision: int | None = None, algo: int | None = None) -> dict:
+    """Solve scenarios held in (pinned) host tensors through the host entry
+    point; the copies run on `stream` (caller synchronises before reading)."""
+    import torch
+    n, K = I.shape
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)
+    o = out if out is not None else _alloc_out(torch, n, K, None, want_w, pin=True)
+    sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end"],
+                            o["order"], o["w"], o["status"])
+    return o

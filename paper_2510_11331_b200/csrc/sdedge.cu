@@ -1,0 +1,915 @@
+// sdedge.cu -- sm_100a kernels and C-ABI implementation of sdedge_solve_batch
+// (include/sdedge.h).  Citations: P:n = PAPER.md line n; DESIGN.md sections.
+//
+// One persistent CTA owns one scenario at a time (atomic work queue):
+//   stage + validate  ->  stable rank sort  ->  t*_com, w* block
+//   reduction (eq:opt_w)  ->  warps pull speculation lengths gamma
+//   from a CTA-local queue and each runs Algorithm 1 for its
+//   gamma  ->  gamma* argmin + backtrack  ->  outputs.
+//
+// Inside one warp's DP, row i's candidates j (lanes) read predecessor row
+// p = j-1.  Upsilon is not stored as a (K+1) x N x 2 table: for n >= 2
+//   Upsilon[p, n, 0] = a0[p] + s0[p] (n-1)            (affine, D2)
+//   Upsilon[p, n, 1] = env_p(n-1), convex piecewise-linear, kept as segments
+// which is exact up to rounding because every stage time is affine in n for
+// n >= 2 (eq:flops_d, eq:flops_v with the KV lengths of P:390).
+// The candidate sum of eq:t_ij1 over n = 2..N is then either
+//   ALGO_ENVELOPE: esum[p] + sum_m max(P + Q m - env_p(m), 0), closed form
+//                  per segment (an arithmetic series on the positive part), or
+//   ALGO_DENSE:    sum_m max(P + Q m, env_p(m)) step by step (the paper's
+//                  O(K^2 N) loop),
+// plus the hoisted verify sum (N-1) Av + Bv (N-1)N/2 and the n = 1 term.
+#include "sdedge.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int code, const char* msg)
+{
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+constexpr int kWarps = 4;                // warps (DP workers) per CTA
+constexpr int kThreads = kWarps * 32;
+
+// ------------------------------------------------------------ call constants
+struct Consts {
+    int K, O_max, gmin, ng;
+    int Jd, hd, h2d, Jv, hv, h2v;
+    double c1d, c2d, c1v, c2v;           // defaults when coeffs == NULL
+    double Bw, sigma2, lambda, dl;
+    long long gamma_s, Gp, kvunit;       // Gamma_s, Gamma_p (eq:memory_model), 4 Jd hd
+    int rows_in_smem;                    // DP row state in shared (1) or global (0) memory
+    long long pool_cap;                  // envelope segments per warp slot
+    long long rows_stride;               // bytes of one warp's global row state
+};
+
+struct Inputs {
+    const int32_t* I;
+    const double* p;
+    const double* g;
+    const double* alpha;
+    const double* coeffs;
+};
+
+struct Outputs {
+    double* lat;
+    int32_t* gamma;
+    int32_t* M;
+    int32_t* bend;
+    int32_t* order;
+    double* w;
+    int32_t* status;
+};
+
+struct Work {
+    unsigned long long* next;      // [2] scenario queue heads (main, big)
+    unsigned int* ovf_count;       // scenarios handed to the big-pool pass
+    long long* ovf_list;           // [n]
+    unsigned char* rows;           // global row state (when not in smem)
+    unsigned char* pool;           // envelope segment pools, one per warp slot
+};
+
+// DP row state of one warp (SoA, generic pointers: smem or global).
+template <typename R>
+struct Rows {
+    R *y0, *y1;        // Upsilon[p, 1, 0], Upsilon[p, 1, 1]
+    R *a0, *s0;        // Upsilon[p, n, 0] = a0 + s0 (n-1), n >= 2
+    R *es;             // sum_{n=2}^{N} Upsilon[p, n, 1]
+    R *la, *ls;        // first envelope segment's line (intercept, slope in m = n-1)
+    int *off, *cnt;    // extra segments pool[off .. off+cnt-2]; cnt = #segments
+};
+
+template <typename R>
+__host__ __device__ inline size_t rows_bytes(int K)
+{
+    return (size_t)(K + 1) * (7 * sizeof(R) + 2 * sizeof(int));
+}
+
+template <typename R>
+__device__ inline Rows<R> carve_rows(unsigned char* base, int K)
+{
+    Rows<R> r;
+    size_t n = (size_t)K + 1;
+    R* f = reinterpret_cast<R*>(base);
+    r.y0 = f; r.y1 = f + n; r.a0 = f + 2 * n; r.s0 = f + 3 * n; r.es = f + 4 * n;
+    r.la = f + 5 * n; r.ls = f + 6 * n;
+    int* q = reinterpret_cast<int*>(f + 7 * n);
+    r.off = q; r.cnt = q + n;
+    return r;
+}
+
+template <typename R>
+struct Pool {
+    int* u;    // first m of the segment
+    R* a;      // intercept
+    R* s;      // slope
+    long long cap;
+};
+
+template <typename R>
+__host__ __device__ inline size_t pool_bytes(long long cap)
+{
+    return (size_t)cap * (sizeof(int) + 2 * sizeof(R));
+}
+
+template <typename R>
+__device__ inline Pool<R> carve_pool(unsigned char* base, long long cap)
+{
+    Pool<R> p;
+    p.a = reinterpret_cast<R*>(base);
+    p.s = p.a + cap;
+    p.u = reinterpret_cast<int*>(p.s + cap);
+    p.cap = cap;
+    return p;
+}
+
+// ------------------------------------------------------------ small helpers
+template <typename R> __device__ inline R rmax(R a, R b) { return a > b ? a : b; }
+template <typename R> __device__ inline R kinf();
+template <> __device__ inline double kinf<double>() { return __longlong_as_double(0x7ff0000000000000LL); }
+template <> __device__ inline float kinf<float>() { return __int_as_float(0x7f800000); }
+
+__device__ inline double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
+__device__ inline double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// Segment k of row p: [u, v] with line (ea, es).
+template <typename R>
+struct Seg { int u, v; R a, s; };
+
+template <typename R>
+__device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, int k, int c, int Mx)
+{
+    Seg<R> sg;
+    if (k == 0) { sg.u = 1; sg.a = rw.la[p]; sg.s = rw.ls[p]; }
+    else {
+        long long q = rw.off[p] + k - 1;
+        sg.u = pl.u[q]; sg.a = pl.a[q]; sg.s = pl.s[q];
+    }
+    sg.v = (k + 1 < c) ? pl.u[rw.off[p] + k] - 1 : Mx;
+    return sg;
+}
+
+// sum_{m=u}^{v} max(dP + dQ m, 0): the positive part of a linear function on
+// an integer range is a single sub-range (one sign change at most).
+template <typename R>
+__device__ inline R pos_sum(R dP, R dQ, int u, int v)
+{
+    R Du = fma(dQ, (R)u, dP), Dv = fma(dQ, (R)v, dP);
+    if (Du <= (R)0 && Dv <= (R)0) return (R)0;
+    if (Du > (R)0 && Dv > (R)0) return (R)(v - u + 1) * (Du + Dv) * (R)0.5;
+    float x = (float)(-dP) / (float)dQ;      // crossing estimate; fixed up exactly below
+    x = fminf(fmaxf(x, (float)u), (float)v);
+    if (Dv > (R)0) {                         // increasing: positive on [f, v], f in (u, v]
+        int f = (int)floorf(x) + 1;
+        f = min(max(f, u + 1), v);
+        while (f > u + 1 && fma(dQ, (R)(f - 1), dP) > (R)0) --f;
+        while (f < v && fma(dQ, (R)f, dP) <= (R)0) ++f;
+        R Df = fma(dQ, (R)f, dP);
+        return (R)(v - f + 1) * (Df + Dv) * (R)0.5;
+    } else {                                 // decreasing: positive on [u, l], l in [u, v)
+        int l = (int)ceilf(x) - 1;
+        l = min(max(l, u), v - 1);
+        while (l < v - 1 && fma(dQ, (R)(l + 1), dP) > (R)0) ++l;
+        while (l > u && fma(dQ, (R)l, dP) <= (R)0) --l;
+        R Dl = fma(dQ, (R)l, dP);
+        return (R)(l - u + 1) * (Du + Dl) * (R)0.5;
+    }
+}
+
+// First / last integer m in [u, v] with dP + dQ m > 0 (caller knows one exists).
+template <typename R>
+__device__ inline int first_pos(R dP, R dQ, int u, int v)
+{
+    if (fma(dQ, (R)u, dP) > (R)0) return u;
+    int f = u + 1;
+    float x = (float)(-dP) / (float)dQ;
+    x = fminf(fmaxf(x, (float)u), (float)v);
+    f = min(max((int)floorf(x) + 1, u + 1), v);
+    while (f > u + 1 && fma(dQ, (R)(f - 1), dP) > (R)0) --f;
+    while (f < v && fma(dQ, (R)f, dP) <= (R)0) ++f;
+    return f;
+}
+
+template <typename R>
+__device__ inline int last_pos(R dP, R dQ, int u, int v)
+{
+    if (fma(dQ, (R)v, dP) > (R)0) return v;
+    float x = (float)(-dP) / (float)dQ;
+    x = fminf(fmaxf(x, (float)u), (float)v);
+    int l = min(max((int)ceilf(x) - 1, u), v - 1);
+    while (l < v - 1 && fma(dQ, (R)(l + 1), dP) > (R)0) ++l;
+    while (l > u && fma(dQ, (R)l, dP) <= (R)0) --l;
+    return l;
+}
+
+// sum_{m=m0}^{m1} max(P + Q m, env_p(m)), one step at a time (eq:t_ij1 as
+// written: the O(N) inner loop of Alg. 1 line 15).  Flat loop so that lanes
+// with different segment boundaries stay converged.
+template <typename R>
+__device__ inline R dense_sum(const Rows<R>& rw, const Pool<R>& pl, int p, R P, R Q, int m0, int m1, int Mx)
+{
+    R acc = (R)0;
+    if (m0 > m1) return acc;
+    const int cntp = rw.cnt[p];
+    int k = 0;
+    Seg<R> sg = get_seg(rw, pl, p, 0, cntp, Mx);
+    while (sg.v < m0) { ++k; sg = get_seg(rw, pl, p, k, cntp, Mx); }
+    R x = (R)m0;
+    for (int m = m0; m <= m1; ++m) {
+        if (m > sg.v) { ++k; sg = get_seg(rw, pl, p, k, cntp, Mx); }
+        acc += rmax(fma(Q, x, P), fma(sg.s, x, sg.a));
+        x += (R)1;
+    }
+    return acc;
+}
+
+// Warp-uniform per-row stage-time coefficients (per unit batch size b) for
+// sorted position i with padded length I: Appendix-A closed forms of
+// eq:d_latency / eq:v_latency summed over the draft passes (D1).
+struct RowCoef {
+    double td1, ad, bd;   // draft: n = 1 value, n >= 2 intercept, slope  (x b)
+    double tv1, av, bv;   // verify (x b)
+    double c2dg, c2vv;    // gamma c2d, c2v + downlink  (not x b)
+};
+
+__device__ inline RowCoef row_coef(const Consts& C, double c1d, double c2d, double c1v, double c2v,
+                                   int gamma, double L, int I)
+{
+    RowCoef r;
+    const double g = gamma, Id = I;
+    const double kd = c1d * (4.0 * C.Jd * (double)C.hd);
+    const double kv = c1v * (4.0 * C.Jv * (double)C.hv);
+    const double hd2 = 2.0 * C.hd + C.h2d, hv2 = 2.0 * C.hv + C.h2v;
+    if (gamma > 0) {
+        const double tri = g * (g - 1.0) * 0.5;               // sum_{i=1}^{g} (i-1)
+        r.td1 = kd * (Id * (hd2 + Id) + (g - 1.0) * (hd2 + Id) + tri);
+        r.ad = kd * (g * (hd2 + Id) + tri);
+        r.bd = kd * g * L;
+    } else {
+        r.td1 = r.ad = r.bd = 0.0;                            // gamma = 0: no draft passes
+    }
+    r.tv1 = kv * (Id + g) * (hv2 + Id + g);
+    r.av = kv * (1.0 + g) * (hv2 + Id + g);
+    r.bv = kv * (1.0 + g) * L;
+    r.c2dg = g * c2d;
+    r.c2vv = c2v + C.dl;
+    return r;
+}
+
+// Candidate data of (i, j) with b = i - j + 1 for predecessor row p = j - 1.
+template <typename R>
+struct Cand { R d0, d1, P, Q, Av, Bv; };
+
+template <typename R>
+__device__ inline Cand<R> cand_terms(const Rows<R>& rw, const RowCoef& rc, int p, int b)
+{
+    const double bd = b;
+    Cand<R> c;
+    const R Td1 = (R)fma(bd, rc.td1, rc.c2dg);
+    const R Tv1 = (R)fma(bd, rc.tv1, rc.c2vv);
+    const R Ad = (R)fma(bd, rc.ad, rc.c2dg);
+    const R Bd = (R)(bd * rc.bd);
+    c.Av = (R)fma(bd, rc.av, rc.c2vv);
+    c.Bv = (R)(bd * rc.bv);
+    c.d0 = rw.y0[p] + Td1;                       // eq:tt1 at n = 1
+    c.d1 = rmax(c.d0, rw.y1[p]) + Tv1;           // eq:tt2 at n = 1 (reading A1)
+    c.P = rw.a0[p] + Ad;                         // Upsilon0 line of the candidate, n >= 2
+    c.Q = rw.s0[p] + Bd;
+    return c;
+}
+
+// Exact IEEE sequence shared with the oracle (reading A2):
+// A = alpha^{gamma+1} by repeated multiplication, L = (1-A)/(1-alpha), N = ceil(O/L).
+__device__ inline double expected_tokens(double alpha, int gamma)
+{
+    double A = alpha;
+    for (int t = 0; t < gamma; ++t) A = __dmul_rn(A, alpha);
+    return __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(1.0, alpha));
+}
+
+// ------------------------------------------------------------ shared layout
+struct Smem {
+    int* I;        // [K] original lengths
+    int* Is;       // [K] sorted lengths
+    int* ord;      // [K] sorted pos -> task
+    short* S;      // [ng][K] boundaries (1-based j*)
+    double* tinf;  // [ng]
+    double* red;   // [2 * kWarps]
+    int* ctl;      // [0] gamma queue, [1] overflow flag, [2] scenario status, [3] bad flag
+    long long* sid;
+    unsigned char* rows; // [kWarps] row states when rows_in_smem
+};
+
+template <typename R>
+__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
+{
+    size_t b = 0;
+    b += 3 * (size_t)K * sizeof(int);
+    b += (size_t)ng * K * sizeof(short);
+    b = (b + 15) & ~(size_t)15;
+    b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
+    b = (b + 15) & ~(size_t)15;
+    if (rows_in_smem) b += kWarps * rows_bytes<R>(K);
+    return b;
+}
+
+__device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
+{
+    Smem s;
+    size_t b = 0;
+    s.I = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
+    s.Is = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
+    s.ord = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
+    s.S = reinterpret_cast<short*>(base + b); b += (size_t)ng * K * sizeof(short);
+    b = (b + 15) & ~(size_t)15;
+    s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
+    s.red = reinterpret_cast<double*>(base + b); b += 2 * kWarps * sizeof(double);
+    s.sid = reinterpret_cast<long long*>(base + b); b += 2 * sizeof(long long);
+    s.ctl = reinterpret_cast<int*>(base + b); b += 8 * sizeof(int);
+    b = (b + 15) & ~(size_t)15;
+    s.rows = base + b;
+    return s;
+}
+
+// ------------------------------------------------------------ the DP of one gamma
+// Returns T_inf (= Upsilon[K,0,0]) or +inf if some row has no feasible batch;
+// sets *overflow if the segment pool ran out.  S[i-1] = j* (1-based).
+template <typename R, int ALGO>
+__device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> pl, int gamma,
+                           double alpha, double c1d, double c2d, double c1v, double c2v,
+                           short* S, bool* overflow)
+{
+    const int lane = threadIdx.x & 31;
+    const int K = C.K;
+    const double L = expected_tokens(alpha, gamma);
+    const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
+    const int Mx = N - 1;                                        // n >= 2 <-> m = n-1 in [1, Mx]
+    const R sumM = (R)((double)Mx * (double)(Mx + 1) * 0.5);
+    long long top = 0;                                           // pool bump pointer
+
+    if (lane == 0) {                                             // row 0 == 0 (reading A3)
+        rw.y0[0] = rw.y1[0] = rw.a0[0] = rw.s0[0] = rw.es[0] = (R)0;
+        rw.la[0] = rw.ls[0] = (R)0;
+        rw.off[0] = 0;
+        rw.cnt[0] = Mx >= 1 ? 1 : 0;
+    }
+    __syncwarp();
+
+    const long long room = C.gamma_s - C.Gp;
+    double T_last = 0.0;
+    int row_ovf = 0;
+    for (int i = 1; i <= K; ++i) {
+        const int I = sm.Is[i - 1];
+        // memory window (Alg. 1 lines 10-13): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
+        long long bmax = room >= 0 ? room / (C.kvunit * ((long long)I + C.O_max)) : 0;
+        const int jlo = bmax >= i ? 1 : (int)(i - bmax + 1);
+        if (jlo > i) { T_last = dinf(); break; }
+        const RowCoef rc = row_coef(C, c1d, c2d, c1v, c2v, gamma, L, I);
+
+        R bT = kinf<R>();
+        int bj = -1;
+        R brest = (R)0;
+        const int nc = i - jlo + 1;
+        if (ALGO == SDEDGE_ALGO_ENVELOPE || nc >= 17) {
+            // one lane per candidate, ascending j per lane
+            for (int j = jlo + lane; j <= i; j += 32) {
+                const int p = j - 1, b = i - j + 1;
+                const Cand<R> c = cand_terms(rw, rc, p, b);
+                R acc;
+                const int cntp = rw.cnt[p];
+                if (ALGO == SDEDGE_ALGO_ENVELOPE) {
+                    acc = rw.es[p];
+                    for (int k = 0; k < cntp; ++k) {
+                        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+                        acc += pos_sum(c.P - sg.a, c.Q - sg.s, sg.u, sg.v);
+                    }
+                } else {
+                    acc = dense_sum(rw, pl, p, c.P, c.Q, 1, Mx, Mx);
+                }
+                const R rest = acc + fma(c.Bv, sumM, (R)Mx * c.Av);
+                const R T = c.d1 + rest;
+                if (T <= bT) { bT = T; bj = j; brest = rest; }   // '>=' of Alg. 1 line 21
+            }
+        } else {
+            // DENSE with few candidates: gsz lanes share one candidate's n-range
+            int gsz = 1;
+            while (gsz * 2 * nc <= 32) gsz *= 2;
+            const int ci = lane / gsz, sub = lane % gsz;
+            R rest = (R)0;
+            int j = -1;
+            Cand<R> c;
+            if (ci < nc) {
+                j = jlo + ci;
+                const int p = j - 1, b = i - j + 1;
+                c = cand_terms(rw, rc, p, b);
+                const int chunk = (Mx + gsz - 1) / gsz;
+                const int m0 = 1 + sub * chunk, m1 = min(Mx, m0 + chunk - 1);
+                const R acc = dense_sum(rw, pl, p, c.P, c.Q, m0, m1, Mx);
+                rest = acc;
+            }
+            for (int o = gsz >> 1; o > 0; o >>= 1) rest += __shfl_xor_sync(0xffffffffu, rest, o);
+            if (ci < nc && sub == 0) {
+                rest = rest + fma(c.Bv, sumM, (R)Mx * c.Av);
+                bT = c.d1 + rest;
+                bj = j;
+                brest = rest;
+            }
+        }
+        // warp argmin over (T, j): smaller T, then larger j (reading A6)
+        R t = bT;
+        int jj = bj;
+        for (int o = 16; o > 0; o >>= 1) {
+            const R ot = __shfl_xor_sync(0xffffffffu, t, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, jj, o);
+            if (ot < t || (ot == t && oj > jj)) { t = ot; jj = oj; }
+        }
+        if (jj < 0) { T_last = dinf(); break; }               // no finite candidate
+        const unsigned own = __ballot_sync(0xffffffffu, bj == jj);
+        const int src = __ffs(own) - 1;
+        const R rest_star = __shfl_sync(0xffffffffu, brest, src);
+
+        if (lane == 0) {
+            // eq:rg, eq:tt1, eq:tt2 with j* (reading A4: S[i] always set)
+            S[i - 1] = (short)jj;
+            const int p = jj - 1, b = i - jj + 1;
+            const Cand<R> c = cand_terms(rw, rc, p, b);
+            rw.y0[i] = c.d0;
+            rw.y1[i] = c.d1;
+            rw.a0[i] = c.P;
+            rw.s0[i] = c.Q;
+            rw.es[i] = rest_star;
+            // env_i(m) = max(P + Q m, env_p(m)) + Av + Bv m.  The positive set of
+            // (line - env_p) is one interval [mlo, mhi] (env_p convex).
+            const int cntp = rw.cnt[p];
+            int mlo = 0, mhi = -1;
+            for (int k = 0; k < cntp && mlo == 0; ++k) {
+                const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+                const R dP = c.P - sg.a, dQ = c.Q - sg.s;
+                if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0)
+                    mlo = first_pos(dP, dQ, sg.u, sg.v);
+            }
+            if (mlo > 0)
+                for (int k = cntp - 1; k >= 0; --k) {
+                    const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+                    const R dP = c.P - sg.a, dQ = c.Q - sg.s;
+                    if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0) {
+                        mhi = last_pos(dP, dQ, sg.u, sg.v);
+                        break;
+                    }
+                }
+            int nseg = 0;
+            const long long base = top;
+            bool ovf = false;
+            auto emit = [&](int u, R a, R s) {
+                a += c.Av;
+                s += c.Bv;
+                if (nseg == 0) { rw.la[i] = a; rw.ls[i] = s; }
+                else {
+                    const long long q = base + nseg - 1;
+                    if (q >= pl.cap) { ovf = true; }
+                    else { pl.u[q] = u; pl.a[q] = a; pl.s[q] = s; }
+                }
+                ++nseg;
+            };
+            bool line_done = false;
+            for (int k = 0; k < cntp; ++k) {
+                const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+                if (mlo > 0 && sg.v >= mlo && sg.u <= mhi) {
+                    if (sg.u < mlo) emit(sg.u, sg.a, sg.s);          // left remainder
+                    if (!line_done) { emit(mlo, c.P, c.Q); line_done = true; }
+                    if (sg.v > mhi) emit(mhi + 1, sg.a, sg.s);       // right remainder
+                } else {
+                    emit(sg.u, sg.a, sg.s);
+                }
+            }
+            rw.off[i] = (int)base;
+            rw.cnt[i] = nseg;
+            top = base + (nseg > 1 ? nseg - 1 : 0);
+            row_ovf = ovf;
+        }
+        top = __shfl_sync(0xffffffffu, top, 0);
+        row_ovf = __shfl_sync(0xffffffffu, row_ovf, 0);
+        __syncwarp();
+        if (row_ovf) { *overflow = true; T_last = dinf(); break; }
+        T_last = (double)t;
+    }
+    return T_last;
+}
+
+// ------------------------------------------------------------ the fused kernel
+template <typename R, int ALGO, int BIG>
+__global__ void __launch_bounds__(kThreads)
+solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = C.K, ng = C.ng;
+    const Smem sm = carve_smem(smem_raw, K, ng);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long slot = (long long)blockIdx.x * kWarps + warp;
+
+    Rows<R> rw = carve_rows<R>(C.rows_in_smem ? sm.rows + (size_t)warp * rows_bytes<R>(K)
+                                              : ws.rows + (size_t)slot * C.rows_stride, K);
+    Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
+    const long long n_items = BIG ? (long long)*ws.ovf_count : n;
+    __shared__ bool s_ovf;
+
+    for (;;) {
+        if (tid == 0) {
+            const unsigned long long it = atomicAdd(ws.next + BIG, 1ULL);
+            sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
+            sm.ctl[0] = 0;
+            s_ovf = false;
+        }
+        __syncthreads();
+        const long long s = sm.sid[0];
+        if (s < 0) break;
+
+        // ---- stage + validate (SoA, coalesced)
+        const int32_t* Ig = in.I + s * K;
+        const double* pg = in.p + s * K;
+        const double* gg = in.g + s * K;
+        int bad = 0;
+        for (int k = tid; k < K; k += kThreads) {
+            const int Ik = Ig[k];
+            const double pk = pg[k], gk = gg[k];
+            sm.I[k] = Ik;
+            if (Ik < 1 || !(pk > 0.0) || !(gk > 0.0) || !isfinite(pk) || !isfinite(gk)) bad = 1;
+        }
+        bad = __syncthreads_or(bad);
+        // ---- stable ascending sort by I_k (reading A13): rank = #{smaller or equal-and-earlier}
+        for (int k = tid; k < K; k += kThreads) {
+            const int Ik = sm.I[k];
+            int r = 0;
+            for (int q = 0; q < K; ++q) {
+                const int Iq = sm.I[q];
+                r += (Iq < Ik) || (Iq == Ik && q < k);
+            }
+            sm.ord[r] = k;
+            sm.Is[r] = Ik;
+        }
+        // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2)
+        double tc = 0.0, q = 0.0;
+        if (!bad)
+            for (int k = tid; k < K; k += kThreads) {
+                const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
+                tc += C.lambda * (double)sm.I[k] / (C.Bw * sk);
+                q += (double)sm.I[k] / sk;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            tc += __shfl_xor_sync(0xffffffffu, tc, o);
+            q += __shfl_xor_sync(0xffffffffu, q, o);
+        }
+        if (lane == 0) { sm.red[warp] = tc; sm.red[kWarps + warp] = q; }
+        __syncthreads();
+        double Tcom = 0.0, qsum = 0.0;
+        for (int w = 0; w < kWarps; ++w) { Tcom += sm.red[w]; qsum += sm.red[kWarps + w]; }
+
+        const double alpha = in.alpha[s];
+        const bool bad_alpha = !(alpha > 0.0 && alpha < 1.0);
+        double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
+        if (in.coeffs) {
+            c1d = in.coeffs[4 * s]; c2d = in.coeffs[4 * s + 1];
+            c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
+        }
+
+        // ---- P3: each warp pulls gamma values and runs Algorithm 1
+        if (!bad && !bad_alpha) {
+            for (;;) {
+                int gi = 0;
+                if (lane == 0) gi = atomicAdd(&sm.ctl[0], 1);
+                gi = __shfl_sync(0xffffffffu, gi, 0);
+                if (gi >= ng) break;
+                bool ovf = false;
+                const double t = dp_gamma<R, ALGO>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
+                                                   sm.S + (size_t)gi * K, &ovf);
+                if (lane == 0) {
+                    sm.tinf[gi] = t;
+                    if (ovf) s_ovf = true;
+                }
+            }
+        }
+        __syncthreads();
+
+        if (s_ovf && !BIG) {
+            // hand the scenario to the big-pool pass (outputs written there)
+            if (tid == 0) {
+                const unsigned int at = atomicAdd(ws.ovf_count, 1u);
+                ws.ovf_list[at] = s;
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- gamma* (smallest argmin, reading A7) and backtrack (reading A5)
+        if (tid == 0) {
+            int st = 0, gbest = -1, M = 0;
+            double best = dinf();
+            if (bad) st = 3;
+            else if (bad_alpha) st = 2;
+            else if (s_ovf) st = 5;          // cannot happen with the worst-case pool
+            else {
+                for (int gi = 0; gi < ng; ++gi)
+                    if (sm.tinf[gi] < best) { best = sm.tinf[gi]; gbest = gi; }
+                if (gbest < 0) st = 1;
+            }
+            double* lat = out.lat + 3 * s;
+            if (st == 0) {
+                const short* S = sm.S + (size_t)gbest * K;
+                int i = K;
+                while (i > 0) { sm.I[M++] = i; i = S[i - 1] - 1; }   // reuse sm.I as a stack
+                lat[0] = Tcom + best; lat[1] = Tcom; lat[2] = best;
+                out.gamma[s] = C.gmin + gbest;
+            } else {
+                const double nan = dnan();
+                lat[0] = st == 1 ? dinf() : nan;
+                lat[1] = st == 3 || st == 5 ? nan : Tcom;
+                lat[2] = st == 1 ? dinf() : nan;
+                out.gamma[s] = -1;
+            }
+            out.M[s] = M;
+            out.status[s] = st;
+            sm.ctl[2] = M;
+            sm.ctl[3] = bad;
+        }
+        __syncthreads();
+        const int M = sm.ctl[2];
+        for (int k = tid; k < K; k += kThreads) {
+            out.order[s * K + k] = sm.ord[k];
+            out.bend[s * K + k] = k < M ? sm.I[M - 1 - k] : 0;
+        }
+        if (out.w)
+            for (int k = tid; k < K; k += kThreads) {
+                double wk = dnan();
+                if (!sm.ctl[3]) {
+                    const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
+                    wk = ((double)Ig[k] / sk) / qsum;
+                }
+                out.w[s * K + k] = wk;
+            }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ pipe-peak microbenchmark
+template <typename T>
+__global__ void pipe_peak_kernel(T* sink, int iters, T seed)
+{
+    T a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+      a6 = a0 + 6, a7 = a0 + 7;
+    const T m = (T)0.999999, c = (T)1e-7;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    const T r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == (T)-1) sink[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
+// ------------------------------------------------------------ host side
+int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const double* lat,
+             const sdedge_schedule* o)
+{
+    if (!s || !p || !o) return fail(-1, "null argument");
+    if (n < 0) return fail(-1, "n < 0");
+    if (p->K < 1 || p->K > SDEDGE_MAX_K) return fail(-1, "K outside 1..1024");
+    if (p->gamma_min < 0 || p->gamma_max < p->gamma_min || p->gamma_max > 64)
+        return fail(-1, "need 0 <= gamma_min <= gamma_max <= 64");
+    if (p->O_max < 1 || p->O_max > (1 << 20)) return fail(-1, "O_max outside 1..2^20");
+    const sdedge_model* ms[2] = {&p->draft, &p->verify};
+    for (const sdedge_model* m : ms)
+        if (m->layers < 1 || m->layers > 1024 || m->hidden < 1 || m->hidden > 65536 || m->ffn < 1 ||
+            m->ffn > (1 << 20))
+            return fail(-1, "model dims outside J in 1..1024, h1 in 1..65536, h2 in 1..2^20");
+    const double cs[4] = {p->c1_draft, p->c2_draft, p->c1_verify, p->c2_verify};
+    for (double c : cs)
+        if (!(c >= 0.0) || !std::isfinite(c)) return fail(-1, "runtime coefficients must be finite and >= 0");
+    if (!(p->bandwidth_hz > 0) || !std::isfinite(p->bandwidth_hz)) return fail(-1, "bandwidth_hz must be > 0");
+    if (!(p->noise_w > 0) || !std::isfinite(p->noise_w)) return fail(-1, "noise_w must be > 0");
+    if (!std::isfinite(p->lambda_bits)) return fail(-1, "lambda_bits must be finite");
+    if (p->mem_capacity_bytes < 0) return fail(-1, "mem_capacity_bytes < 0");
+    if (p->precision != 0 && p->precision != 1) return fail(-1, "precision must be 0 (fp64) or 1 (fp32)");
+    if (p->algo != SDEDGE_ALGO_ENVELOPE && p->algo != SDEDGE_ALGO_DENSE) return fail(-1, "unknown algo");
+    if (p->flags & ~SDEDGE_FLAG_TINY_POOL) return fail(-1, "unknown flags");
+    if (!(p->downlink_s >= 0) || !std::isfinite(p->downlink_s)) return fail(-1, "downlink_s must be >= 0");
+    if (n > 0) {
+        if (!s->input_len || !s->tx_power_w || !s->gain || !s->alpha) return fail(-1, "null scenario array");
+        if (!lat || !o->gamma || !o->num_batches || !o->batch_end || !o->order || !o->status)
+            return fail(-1, "null output array");
+    }
+    return 0;
+}
+
+#define CU(x)                                                                   \
+    do {                                                                        \
+        cudaError_t e_ = (x);                                                   \
+        if (e_ != cudaSuccess) {                                                \
+            snprintf(g_err, sizeof(g_err), "%s: %s", #x, cudaGetErrorString(e_)); \
+            return e_ == cudaErrorMemoryAllocation ? -3 : -2;                   \
+        }                                                                       \
+    } while (0)
+
+template <typename R, int ALGO>
+int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long n, cudaStream_t st, int flags)
+{
+    int dev = 0, nsm = 0, max_smem = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+
+    Consts C = C0;
+    const size_t rb = rows_bytes<R>(C.K);
+    // row state in shared memory when it keeps >= 3 CTAs (12 warps) per SM
+    C.rows_in_smem = smem_bytes<R>(C.K, C.ng, 1) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
+    const size_t sb = smem_bytes<R>(C.K, C.ng, C.rows_in_smem);
+    if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
+    C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
+
+    auto k_main = solve_kernel<R, ALGO, 0>;
+    auto k_big = solve_kernel<R, ALGO, 1>;
+    CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_main, kThreads, sb));
+    if (occ < 1) return fail(-1, "kernel does not fit on an SM");
+    long long grid = (long long)nsm * occ;
+    if (grid > n) grid = n;
+
+    // typical envelopes have <= a few segments per row: 4 (K+1) + 64 extra
+    // segments per warp; a DP that overflows is redone by the big-pool pass
+    // with the worst-case bound sum_i 2i = K(K+1) (D3).
+    const long long cap_main = (flags & SDEDGE_FLAG_TINY_POOL) ? 8LL : (4LL * (C.K + 1) + 64 + 7) & ~7LL;
+    const long long cap_big = ((long long)C.K * (C.K + 1) + 64 + 7) & ~7LL;
+    long long grid_big = std::max(1LL, std::min((long long)nsm,
+                                  (2LL << 30) / (long long)(kWarps * pool_bytes<R>(cap_big))));
+    const long long slots = grid * kWarps, slots_big = grid_big * kWarps;
+
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+    const size_t o_next = take(2 * sizeof(unsigned long long) + sizeof(unsigned int));
+    const size_t o_list = take((size_t)n * sizeof(long long));
+    const size_t o_rows = take(C.rows_in_smem ? 0 : (size_t)std::max(slots, slots_big) * C.rows_stride);
+    const size_t o_pool = take((size_t)slots * pool_bytes<R>(cap_main));
+    const size_t o_pool_big = take((size_t)slots_big * pool_bytes<R>(cap_big));
+    unsigned char* wsb = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&wsb), off, st));
+    CU(cudaMemsetAsync(wsb + o_next, 0, 2 * sizeof(unsigned long long) + sizeof(unsigned int), st));
+
+    Work w;
+    w.next = reinterpret_cast<unsigned long long*>(wsb + o_next);
+    w.ovf_count = reinterpret_cast<unsigned int*>(wsb + o_next + 2 * sizeof(unsigned long long));
+    w.ovf_list = reinterpret_cast<long long*>(wsb + o_list);
+    w.rows = wsb + o_rows;
+
+    int launches = 0;
+    if (n > 0) {
+        C.pool_cap = cap_main;
+        w.pool = wsb + o_pool;
+        k_main<<<(unsigned)grid, kThreads, sb, st>>>(C, in, out, n, w);
+        ++launches;
+        CU(cudaGetLastError());
+        C.pool_cap = cap_big;
+        w.pool = wsb + o_pool_big;
+        k_big<<<(unsigned)grid_big, kThreads, sb, st>>>(C, in, out, n, w);
+        ++launches;
+        CU(cudaGetLastError());
+    }
+    CU(cudaFreeAsync(wsb, st));
+    g_launches = launches;
+    return 0;
+}
+
+int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* lat,
+                 sdedge_schedule* o)
+{
+    Consts C{};
+    C.K = p->K; C.O_max = p->O_max; C.gmin = p->gamma_min; C.ng = p->gamma_max - p->gamma_min + 1;
+    C.Jd = p->draft.layers; C.hd = p->draft.hidden; C.h2d = p->draft.ffn;
+    C.Jv = p->verify.layers; C.hv = p->verify.hidden; C.h2v = p->verify.ffn;
+    C.c1d = p->c1_draft; C.c2d = p->c2_draft; C.c1v = p->c1_verify; C.c2v = p->c2_verify;
+    C.Bw = p->bandwidth_hz; C.sigma2 = p->noise_w;
+    C.lambda = p->lambda_bits > 0 ? p->lambda_bits : 16.0 * ((double)C.hd + (double)C.hv);
+    C.dl = p->downlink_s;
+    C.gamma_s = p->mem_capacity_bytes;
+    C.Gp = (long long)C.Jd * (8LL * C.hd * C.hd + 4LL * C.hd * C.h2d);                      // eq:memory_model
+    C.kvunit = 4LL * C.Jd * C.hd;                                                            // eq:memory_kv
+    Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
+    Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status};
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    if (p->precision == 0)
+        return p->algo == SDEDGE_ALGO_DENSE ? launch_all<double, SDEDGE_ALGO_DENSE>(C, in, out, n, st, p->flags)
+                                            : launch_all<double, SDEDGE_ALGO_ENVELOPE>(C, in, out, n, st, p->flags);
+    return p->algo == SDEDGE_ALGO_DENSE ? launch_all<float, SDEDGE_ALGO_DENSE>(C, in, out, n, st, p->flags)
+                                        : launch_all<float, SDEDGE_ALGO_ENVELOPE>(C, in, out, n, st, p->flags);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ exported C ABI
+extern "C" {
+
+int sdedge_abi_version(void) { return SDEDGE_ABI_VERSION; }
+
+const char* sdedge_last_error(void) { return g_err; }
+
+int sdedge_last_launch_count(void) { return g_launches; }
+
+int sdedge_solve_batch(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
+                       sdedge_schedule* o)
+{
+    g_err[0] = 0;
+    g_launches = 0;
+    int rc = validate(s, n, p, out_latency, o);
+    if (rc) return rc;
+    return solve_device(s, n, p, out_latency, o);
+}
+
+int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
+                            sdedge_schedule* o)
+{
+    g_err[0] = 0;
+    g_launches = 0;
+    int rc = validate(s, n, p, out_latency, o);
+    if (rc) return rc;
+    if (n == 0) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    const size_t K = (size_t)p->K, nn = (size_t)n;
+    const size_t bI = nn * K * 4, bD = nn * K * 8, bA = nn * 8, bC = s->coeffs ? nn * 32 : 0;
+    const size_t bLat = nn * 24, bS = nn * 4, bW = o->bw_share ? nn * K * 8 : 0;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t q = off; off += (b + 255) & ~(size_t)255; return q; };
+    const size_t oI = take(bI), oP = take(bD), oG = take(bD), oA = take(bA), oC = take(bC);
+    const size_t oLat = take(bLat), oGm = take(bS), oM = take(bS), oBe = take(bI), oOr = take(bI),
+                 oW = take(bW), oSt = take(bS);
+    unsigned char* d = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d), off, st));
+    CU(cudaMemcpyAsync(d + oI, s->input_len, bI, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d + oP, s->tx_power_w, bD, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d + oG, s->gain, bD, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(d + oA, s->alpha, bA, cudaMemcpyHostToDevice, st));
+    if (bC) CU(cudaMemcpyAsync(d + oC, s->coeffs, bC, cudaMemcpyHostToDevice, st));
+    sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI), reinterpret_cast<double*>(d + oP),
+                        reinterpret_cast<double*>(d + oG), reinterpret_cast<double*>(d + oA),
+                        bC ? reinterpret_cast<double*>(d + oC) : nullptr};
+    sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm), reinterpret_cast<int32_t*>(d + oM),
+                         reinterpret_cast<int32_t*>(d + oBe), reinterpret_cast<int32_t*>(d + oOr),
+                         bW ? reinterpret_cast<double*>(d + oW) : nullptr, reinterpret_cast<int32_t*>(d + oSt)};
+    rc = solve_device(&ds, n, p, reinterpret_cast<double*>(d + oLat), &dsch);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(out_latency, d + oLat, bLat, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o->gamma, d + oGm, bS, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o->num_batches, d + oM, bS, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o->batch_end, d + oBe, bI, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o->order, d + oOr, bI, cudaMemcpyDeviceToHost, st));
+    if (bW) CU(cudaMemcpyAsync(o->bw_share, d + oW, bW, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o->status, d + oSt, bS, cudaMemcpyDeviceToHost, st));
+    CU(cudaFreeAsync(d, st));
+    return 0;
+}
+
+int sdedge_pipe_peak(int32_t fp32, double* ops_per_s, double* elapsed_s)
+{
+    g_err[0] = 0;
+    if (!ops_per_s) return fail(-1, "null ops_per_s");
+    int dev = 0, nsm = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int threads = 256, blocks = nsm * 8, iters = fp32 ? 8192 : 2048;
+    void* sink = nullptr;
+    CU(cudaMalloc(&sink, (size_t)blocks * threads * 8));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {   // first pass warms clocks
+        CU(cudaEventRecord(e0));
+        if (fp32) pipe_peak_kernel<float><<<blocks, threads>>>((float*)sink, iters, 1.0f);
+        else pipe_peak_kernel<double><<<blocks, threads>>>((double*)sink, iters, 1.0);
+        CU(cudaEventRecord(e1));
+        CU(cudaEventSynchronize(e1));
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+    }
+    CU(cudaEventDestroy(e0));
+    CU(cudaEventDestroy(e1));
+    CU(cudaFree(sink));
+    const double ops = (double)blocks * threads * iters * 16.0 * 8.0;
+    *ops_per_s = ops / (ms * 1e-3);
+    if (elapsed_s) *elapsed_s = ms * 1e-3;
+    return 0;
+}
+
+}  // extern "C"

@@ -94,8 +94,13 @@ def params(pair: str = "68M-7B", K: int = 128, gamma_min: int = 1, gamma_max: in
 
 def generate(root: int, K: int, s0: int, s1: int, I_max: int = 512,
              alpha_lo: float = 0.5, alpha_hi: float = 0.9, tx_power_w: float = 0.2,
-             g0: float = 1e-3, radius_m: float = 400.0) -> dict:
+             g0: float = 1e-3, radius_m: float = 400.0, chunk: int = 1 << 15) -> dict:
     """Scenarios s0..s1-1 of root seed `root` (SoA numpy arrays)."""
+    if s1 - s0 > chunk:
+        parts = [generate(root, K, a, min(a + chunk, s1), I_max, alpha_lo, alpha_hi, tx_power_w, g0,
+                          radius_m, chunk) for a in range(s0, s1, chunk)]
+        return {k: (np.concatenate([q[k] for q in parts]) if parts[0][k] is not None else None)
+                for k in parts[0]}
     n = s1 - s0
     s = np.arange(s0, s1, dtype=np.uint64)[:, None]
     k = np.arange(K, dtype=np.uint64)[None, :]

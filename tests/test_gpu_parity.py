@@ -1,0 +1,244 @@
+"""-m gpu: the CUDA path (through the C ABI) against the oracle, element by
+element on the same seeded inputs (tests/parity.py for the tolerances).
+
+Sizes: C1/C2 in full; C3 on a sample spanning many CTAs and ragged rows;
+C4 and C5 solved at FULL size in the bench's launch configuration and
+checked on deterministic samples the oracle can compute one by one, plus
+properties that hold at any size (self-consistency of the plan under the
+literal eq:time evaluation, constraints (a)-(g))."""
+import numpy as np
+import pytest
+
+import oracle
+import scengen
+from tests.parity import compare, gpu_solve, to_numpy
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ENV, DENSE = 0, 1
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_11331_b200 as sd
+    sd.lib()
+    oracle.build()
+
+
+def _check(pd, sc, precision=0, algo=ENV, orc=None, idx=None):
+    orc = orc if orc is not None else oracle.solve_batch(pd, sc)
+    g = gpu_solve(pd, sc, precision=precision, algo=algo, idx=idx)
+    return compare(pd, sc, g, orc, precision, oracle), orc, g
+
+
+# ---------------------------------------------------------------- C1, C2
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B", "1.1B-13B"])
+def test_c1_all(pair):
+    pd, sc, _ = scengen.config("C1", pair=pair)
+    orc = oracle.solve_batch(pd, sc)
+    for prec, algo in ((0, ENV), (0, DENSE), (1, ENV), (1, DENSE)):
+        res, _, g = _check(pd, sc, prec, algo, orc)
+        assert res["failures"] == 0
+    assert g["gamma"][0] == {"68M-7B": 4, "1.1B-7B": 3, "1.1B-13B": g["gamma"][0]}[pair]
+
+
+def test_c1_against_brute_force():
+    """Joint brute force over every contiguous partition and gamma (K = 4): the
+    GPU never beats it, and matches it wherever Algorithm 1 is exact (P8)."""
+    pd, sc, _ = scengen.config("C1", 0, 200, pair="1.1B-13B")
+    g = gpu_solve(pd, sc)
+    n_eq = 0
+    for s in range(200):
+        Is = sc["I"][s][g["order"][s]]
+        bf, bg, plan = oracle.brute_force(pd, Is, float(sc["alpha"][s]), 0, 4)
+        assert g["lat"][s, 2] >= bf * (1 - 1e-12)
+        n_eq += abs(g["lat"][s, 2] - bf) <= 1e-12 * bf
+    assert n_eq >= 150
+
+
+def test_c2_heterogeneous_speeds():
+    pd, sc, _ = scengen.config("C2")
+    orc = oracle.solve_batch(pd, sc)
+    for prec, algo in ((0, ENV), (0, DENSE), (1, ENV)):
+        res, _, _ = _check(pd, sc, prec, algo, orc)
+        assert res["failures"] == 0
+
+
+# ---------------------------------------------------------------- C3
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_c3_sample(pair):
+    _, sc, _ = scengen.config("C3", 0, 1500)
+    pd = scengen.params(pair, K=32, gamma_min=1, gamma_max=8)
+    orc = oracle.solve_batch(pd, sc)
+    res, _, _ = _check(pd, sc, 0, ENV, orc)
+    assert res["exact"] + res["exempt"] == 1500
+    sub = {k: (v[:300] if v is not None else None) for k, v in sc.items()}
+    orc_sub = {k: v[:300] if hasattr(v, "__len__") else v for k, v in orc.items()}
+    _check(pd, sub, 0, DENSE, orc_sub)
+    _check(pd, sub, 1, ENV, orc_sub)
+
+
+# ---------------------------------------------------------------- C4 (bench config)
+def test_c4_full_size_sampled():
+    """All 1e6 C4 scenarios in one call (the bench launch); oracle on a
+    deterministic sample s = 0 mod 62500; invariants on every scenario."""
+    pd, sc, n = scengen.config("C4")
+    g = gpu_solve(pd, sc)
+    idx = np.arange(0, n, 62500)
+    sub = {k: (v[idx] if v is not None else None) for k, v in sc.items()}
+    orc = oracle.solve_batch(pd, sub)
+    res = compare(pd, sc, g, orc, 0, oracle, idx=idx)
+    assert res["failures"] == 0
+    assert np.all(g["status"] == 0)
+    M = g["M"]
+    assert np.all((M >= 1) & (M <= 128)) and np.all((g["gamma"] >= 1) & (g["gamma"] <= 16))
+    assert np.all(g["batch_end"][np.arange(n), M - 1] == 128)
+    assert np.all(g["lat"][:, 0] == g["lat"][:, 1] + g["lat"][:, 2])
+    assert np.allclose(g["w"].sum(1), 1.0, rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- C5 (large K)
+@pytest.mark.parametrize("K", [256, 512, 1024])
+def test_c5_large_k(K):
+    """Full 1e4-scenario launch at each K; oracle on small samples (gamma range
+    reduced for the oracle's literal O(K^2 N gamma) cost) and the eq:time
+    self-consistency of every sampled GPU plan at the full gamma range."""
+    pd, sc, n = scengen.config(f"C5{K}")
+    g = gpu_solve(pd, sc)
+    assert np.all(g["status"] == 0)
+    rng = np.random.default_rng(K)
+    for s in rng.choice(n, 6, replace=False):
+        Is = sc["I"][s][g["order"][s]]
+        ends = list(g["batch_end"][s][: g["M"][s]])
+        v = oracle.eval_plan(pd, Is, float(sc["alpha"][s]), int(g["gamma"][s]), ends)
+        assert abs(v - g["lat"][s, 2]) <= 1e-12 * v
+    n_or = {256: 3, 512: 2, 1024: 1}[K]
+    gmax = {256: 4, 512: 2, 1024: 1}[K]
+    pd2 = dict(pd, gamma_min=1, gamma_max=gmax)
+    sub = {k: (v[:n_or] if v is not None else None) for k, v in sc.items()}
+    res, _, _ = _check(pd2, sub, 0, ENV)
+    assert res["failures"] == 0
+    _check(pd2, {k: (v[:1] if v is not None else None) for k, v in sc.items()}, 0, DENSE)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_k1_and_single_step():
+    for K, O in ((1, 2048), (5, 1), (7, 2)):
+        pd = scengen.params("1.1B-7B", K=K, gamma_min=0, gamma_max=6, O_max=O)
+        sc = scengen.generate(21, K, 0, 64)
+        for algo in (ENV, DENSE):
+            _check(pd, sc, 0, algo)
+
+
+def test_memory_window_and_infeasible():
+    pd = scengen.params("1.1B-7B", K=64, gamma_min=1, gamma_max=4)
+    sc = scengen.generate(22, 64, 0, 40)
+    sc["I"][:20] = np.maximum(sc["I"][:20], 400)  # windows bind hard
+    _check(pd, sc, 0, ENV)
+    pd_bad = dict(pd, mem_capacity_bytes=2_000_000_000)  # 1.1B weights + one KV barely / not fit
+    res, orc, g = _check(pd_bad, sc, 0, ENV)
+    assert np.any(g["status"] == 1)
+    assert np.all(np.isinf(g["lat"][g["status"] == 1, 0]))
+
+
+def test_invalid_scenarios_status():
+    pd = scengen.params("68M-7B", K=8, gamma_min=1, gamma_max=3)
+    sc = scengen.generate(23, 8, 0, 6)
+    sc["alpha"][1] = 1.0
+    sc["alpha"][2] = float("nan")
+    sc["I"][3, 4] = 0
+    sc["g"][4, 0] = -1e-9
+    sc["p"][5, 7] = float("inf")
+    res, orc, g = _check(pd, sc)
+    assert list(g["status"]) == [0, 2, 2, 3, 3, 3]
+
+
+def test_downlink_and_gamma0():
+    pd = scengen.params("68M-7B", K=16, gamma_min=0, gamma_max=3, downlink_s=2.5e-3)
+    sc = scengen.generate(24, 16, 0, 50)
+    _check(pd, sc, 0, ENV)
+    _check(pd, sc, 0, DENSE)
+
+
+def test_exact_ties_largest_j():
+    """All runtime coefficients zero: every candidate ties at exactly 0, so
+    the '>=' rule (largest j) gives M = K singleton batches (reading A6)."""
+    pd = scengen.params("68M-7B", K=12, gamma_min=1, gamma_max=2, c1_draft=0.0, c2_draft=0.0,
+                        c1_verify=0.0, c2_verify=0.0)
+    sc = scengen.generate(25, 12, 0, 8)
+    g = gpu_solve(pd, sc)
+    assert np.all(g["M"] == 12) and np.all(g["gamma"] == 1) and np.all(g["lat"][:, 2] == 0.0)
+    orc = oracle.solve_batch(pd, sc)
+    assert np.array_equal(orc["batch_end"], g["batch_end"])
+
+
+def test_overflow_second_pass():
+    """FLAG_TINY_POOL forces every multi-segment DP through the worst-case
+    second pass; results must be identical to the normal path."""
+    pd = scengen.params("1.1B-7B", K=64, gamma_min=1, gamma_max=8)
+    _, sc, _ = scengen.config("C2")
+    sc = dict(sc)
+    a = gpu_solve(pd, sc)
+    b = gpu_solve(dict(pd, flags=1), sc)
+    for k in a:
+        if a[k] is not None:
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_host_entry_point_and_determinism():
+    import paper_2510_11331_b200 as sd
+    pd, sc, _ = scengen.config("C3", 0, 3000)
+    d1 = gpu_solve(pd, sc)
+    d2 = gpu_solve(pd, sc)
+    I = torch.from_numpy(sc["I"]).pin_memory()
+    p = torch.from_numpy(sc["p"]).pin_memory()
+    g = torch.from_numpy(sc["g"]).pin_memory()
+    al = torch.from_numpy(sc["alpha"]).pin_memory()
+    h = sd.solve_host(pd, I, p, g, al)
+    torch.cuda.synchronize()
+    h = to_numpy(h)
+    for k in d1:
+        assert np.array_equal(d1[k], d2[k]), k
+        assert np.array_equal(d1[k], h[k]), k
+
+
+def test_permutation_invariance():
+    pd, sc, _ = scengen.config("C3", 0, 200)
+    a = gpu_solve(pd, sc)
+    rng = np.random.default_rng(3)
+    perm = np.stack([rng.permutation(32) for _ in range(200)])
+    sc2 = dict(sc, I=np.take_along_axis(sc["I"], perm, 1), p=np.take_along_axis(sc["p"], perm, 1),
+               g=np.take_along_axis(sc["g"], perm, 1))
+    b = gpu_solve(pd, sc2)
+    assert np.allclose(a["lat"], b["lat"], rtol=1e-12, atol=0)
+    assert np.array_equal(a["gamma"], b["gamma"]) and np.array_equal(a["batch_end"], b["batch_end"])
+
+
+def test_streams_and_empty_call():
+    import paper_2510_11331_b200 as sd
+    pd, sc, _ = scengen.config("C3", 0, 500)
+    I = torch.from_numpy(sc["I"]).cuda()
+    p = torch.from_numpy(sc["p"]).cuda()
+    g = torch.from_numpy(sc["g"]).cuda()
+    al = torch.from_numpy(sc["alpha"]).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    o1 = sd.solve(pd, I, p, g, al, stream=s1)
+    o2 = sd.solve(pd, I, p, g, al, stream=s2)
+    torch.cuda.synchronize()
+    for k in o1:
+        if o1[k] is not None:
+            assert torch.equal(o1[k], o2[k])
+    e = sd.solve(pd, I[:0], p[:0], g[:0], al[:0])
+    torch.cuda.synchronize()
+    assert e["lat"].shape == (0, 3)
+    assert sd.sdedge_last_launch_count() == 0
+
+
+def test_pipe_peak_runs():
+    import paper_2510_11331_b200 as sd
+    ops, t = sd.sdedge_pipe_peak(False)
+    assert ops > 1e12 and t > 0
