@@ -44,7 +44,8 @@ class SdedgeScenarios(C.Structure):
 
 class SdedgeSchedule(C.Structure):
     _fields_ = [("gamma", C.c_void_p), ("num_batches", C.c_void_p), ("batch_end", C.c_void_p),
-                ("order", C.c_void_p), ("bw_share", C.c_void_p), ("status", C.c_void_p)]
+                ("order", C.c_void_p), ("bw_share", C.c_void_p), ("status", C.c_void_p),
+                ("work_counters", C.c_void_p)]
 
 
 _lib = None
@@ -106,9 +107,9 @@ def _ptr(t):
     return t.ctypes.data  # numpy (host entry point)
 
 
-def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, status):
+def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, status, work=None):
     sc = SdedgeScenarios(_ptr(I), _ptr(p), _ptr(g), _ptr(alpha), _ptr(coeffs))
-    sch = SdedgeSchedule(_ptr(gamma), _ptr(M), _ptr(bend), _ptr(order), _ptr(w), _ptr(status))
+    sch = SdedgeSchedule(_ptr(gamma), _ptr(M), _ptr(bend), _ptr(order), _ptr(w), _ptr(status), _ptr(work))
     rc = fn(C.byref(sc), n, C.byref(P), _ptr(lat), C.byref(sch))
     if rc != 0:
         raise RuntimeError(f"sdedge_solve_batch failed ({rc}): {sdedge_last_error()}")
@@ -116,10 +117,10 @@ def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, statu
 
 
 def sdedge_solve_batch(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma, num_batches,
-                       batch_end, order, bw_share, status):
+                       batch_end, order, bw_share, status, work_counters=None):
     """Direct C-ABI call on DEVICE tensors (all contiguous, see include/sdedge.h)."""
     return _call(lib().sdedge_solve_batch, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
-                 num_batches, batch_end, order, bw_share, status)
+                 num_batches, batch_end, order, bw_share, status, work_counters)
 
 
 def sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma,
@@ -149,7 +150,7 @@ def _alloc_out(torch, n, K, device, want_w, pin=False):
 
 
 def solve(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream=None, out=None,
-          precision: int | None = None, algo: int | None = None) -> dict:
+          precision: int | None = None, algo: int | None = None, work_counters=None) -> dict:
     """Solve scenarios held in CUDA tensors; returns CUDA output tensors
     (enqueued on `stream`, default torch's current stream)."""
     import torch
@@ -160,7 +161,7 @@ def solve(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream
     P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)
     o = out if out is not None else _alloc_out(torch, n, K, dev, want_w)
     sdedge_solve_batch(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end"],
-                       o["order"], o["w"], o["status"])
+                       o["order"], o["w"], o["status"], work_counters)
     return o
 
 

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "sdedge.cu")
 HDR = os.path.join(ROOT, "include", "sdedge.h")
-LIB = os.path.join(PKG, "libsdedge.so")
+LIB = os.environ.get("SDEDGE_LIB") or os.path.join(PKG, "libsdedge.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
@@ -21,12 +21,14 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = (not os.path.exists(LIB) or
-             os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)))
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    lib = out or LIB
+    stale = (not os.path.exists(lib) or
+             os.path.getmtime(lib) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)))
     if force or stale:
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, SRC]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+               "-o", lib, SRC]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
-    return LIB
+    return lib

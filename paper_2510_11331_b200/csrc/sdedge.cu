@@ -71,6 +71,12 @@ struct Outputs {
     int32_t* order;
     double* w;
     int32_t* status;
+    unsigned long long* work;   // [4] or null: candidates, candidate x segments, candidate-steps, rows
+};
+
+// Work actually evaluated by one lane (reduced per CTA, flushed once at exit).
+struct WorkCount {
+    unsigned long long cand = 0, seg = 0, steps = 0, rows = 0;
 };
 
 struct Work {
@@ -87,14 +93,14 @@ struct Rows {
     R *y0, *y1;        // Upsilon[p, 1, 0], Upsilon[p, 1, 1]
     R *a0, *s0;        // Upsilon[p, n, 0] = a0 + s0 (n-1), n >= 2
     R *es;             // sum_{n=2}^{N} Upsilon[p, n, 1]
-    R *la, *ls;        // first envelope segment's line (intercept, slope in m = n-1)
+    R *la, *ls, *lv;   // first envelope segment: line (intercept, slope in m = n-1), last m
     int *off, *cnt;    // extra segments pool[off .. off+cnt-2]; cnt = #segments
 };
 
 template <typename R>
 __host__ __device__ inline size_t rows_bytes(int K)
 {
-    return (size_t)(K + 1) * (7 * sizeof(R) + 2 * sizeof(int));
+    return (size_t)(K + 1) * (8 * sizeof(R) + 2 * sizeof(int));
 }
 
 template <typename R>
@@ -104,8 +110,8 @@ __device__ inline Rows<R> carve_rows(unsigned char* base, int K)
     size_t n = (size_t)K + 1;
     R* f = reinterpret_cast<R*>(base);
     r.y0 = f; r.y1 = f + n; r.a0 = f + 2 * n; r.s0 = f + 3 * n; r.es = f + 4 * n;
-    r.la = f + 5 * n; r.ls = f + 6 * n;
-    int* q = reinterpret_cast<int*>(f + 7 * n);
+    r.la = f + 5 * n; r.ls = f + 6 * n; r.lv = f + 7 * n;
+    int* q = reinterpret_cast<int*>(f + 8 * n);
     r.off = q; r.cnt = q + n;
     return r;
 }
@@ -144,59 +150,37 @@ template <> __device__ inline float kinf<float>() { return __int_as_float(0x7f80
 __device__ inline double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 __device__ inline double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
-// Segment k of row p: [u, v] with line (ea, es).
-template <typename R>
-struct Seg { int u, v; R a, s; };
-
-template <typename R>
-__device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, int k, int c, int Mx)
+// Warp argmin over (T, j): smallest T, then the LARGEST j (reading A6: the
+// ">=" of Alg. 1 line 21).  T >= 0 or +inf, so its IEEE bit pattern orders
+// like an unsigned integer: three REDUX instructions instead of a shuffle tree.
+__device__ inline int warp_argmin(double t, int j, double* tmin)
 {
-    Seg<R> sg;
-    if (k == 0) { sg.u = 1; sg.a = rw.la[p]; sg.s = rw.ls[p]; }
-    else {
-        long long q = rw.off[p] + k - 1;
-        sg.u = pl.u[q]; sg.a = pl.a[q]; sg.s = pl.s[q];
-    }
-    sg.v = (k + 1 < c) ? pl.u[rw.off[p] + k] - 1 : Mx;
-    return sg;
+    const unsigned long long key = (unsigned long long)__double_as_longlong(t);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+    *tmin = __hiloint2double((int)mhi, (int)mlo);
+    return __reduce_max_sync(0xffffffffu, (hi == mhi && lo == mlo) ? j : -1);
 }
 
-// sum_{m=u}^{v} max(dP + dQ m, 0): the positive part of a linear function on
-// an integer range is a single sub-range (one sign change at most).
-template <typename R>
-__device__ inline R pos_sum(R dP, R dQ, int u, int v)
+__device__ inline int warp_argmin(float t, int j, float* tmin)
 {
-    R Du = fma(dQ, (R)u, dP), Dv = fma(dQ, (R)v, dP);
-    if (Du <= (R)0 && Dv <= (R)0) return (R)0;
-    if (Du > (R)0 && Dv > (R)0) return (R)(v - u + 1) * (Du + Dv) * (R)0.5;
-    float x = (float)(-dP) / (float)dQ;      // crossing estimate; fixed up exactly below
-    x = fminf(fmaxf(x, (float)u), (float)v);
-    if (Dv > (R)0) {                         // increasing: positive on [f, v], f in (u, v]
-        int f = (int)floorf(x) + 1;
-        f = min(max(f, u + 1), v);
-        while (f > u + 1 && fma(dQ, (R)(f - 1), dP) > (R)0) --f;
-        while (f < v && fma(dQ, (R)f, dP) <= (R)0) ++f;
-        R Df = fma(dQ, (R)f, dP);
-        return (R)(v - f + 1) * (Df + Dv) * (R)0.5;
-    } else {                                 // decreasing: positive on [u, l], l in [u, v)
-        int l = (int)ceilf(x) - 1;
-        l = min(max(l, u), v - 1);
-        while (l < v - 1 && fma(dQ, (R)(l + 1), dP) > (R)0) ++l;
-        while (l > u && fma(dQ, (R)l, dP) <= (R)0) --l;
-        R Dl = fma(dQ, (R)l, dP);
-        return (R)(l - u + 1) * (Du + Dl) * (R)0.5;
-    }
+    const unsigned key = __float_as_uint(t);
+    const unsigned m = __reduce_min_sync(0xffffffffu, key);
+    *tmin = __uint_as_float(m);
+    return __reduce_max_sync(0xffffffffu, key == m ? j : -1);
 }
 
-// First / last integer m in [u, v] with dP + dQ m > 0 (caller knows one exists).
+// First / last integer m in [u, v] with dP + dQ m > 0, given that the sign
+// changes inside [u, v] (exactly once: the function is linear).  A float
+// estimate of the crossing is fixed up with exact comparisons.
 template <typename R>
 __device__ inline int first_pos(R dP, R dQ, int u, int v)
 {
     if (fma(dQ, (R)u, dP) > (R)0) return u;
-    int f = u + 1;
     float x = (float)(-dP) / (float)dQ;
     x = fminf(fmaxf(x, (float)u), (float)v);
-    f = min(max((int)floorf(x) + 1, u + 1), v);
+    int f = min(max((int)floorf(x) + 1, u + 1), v);
     while (f > u + 1 && fma(dQ, (R)(f - 1), dP) > (R)0) --f;
     while (f < v && fma(dQ, (R)f, dP) <= (R)0) ++f;
     return f;
@@ -212,6 +196,41 @@ __device__ inline int last_pos(R dP, R dQ, int u, int v)
     while (l < v - 1 && fma(dQ, (R)(l + 1), dP) > (R)0) ++l;
     while (l > u && fma(dQ, (R)l, dP) <= (R)0) --l;
     return l;
+}
+
+// sum_{m=u}^{v} max(dP + dQ m, 0): the positive part of a linear function on
+// an integer range is one sub-range, summed as an arithmetic series.
+template <typename R>
+__device__ inline R pos_sum(R dP, R dQ, R u, R v)
+{
+    const R Du = fma(dQ, u, dP), Dv = fma(dQ, v, dP);
+    if (Du <= (R)0 && Dv <= (R)0) return (R)0;
+    if (Du > (R)0 && Dv > (R)0) return (v - u + (R)1) * (Du + Dv) * (R)0.5;
+    const int ui = (int)u, vi = (int)v;
+    if (Dv > (R)0) {                         // increasing: positive on [f, v]
+        const int f = first_pos(dP, dQ, ui, vi);
+        return (R)(vi - f + 1) * (fma(dQ, (R)f, dP) + Dv) * (R)0.5;
+    }
+    const int l = last_pos(dP, dQ, ui, vi);  // decreasing: positive on [u, l]
+    return (R)(l - ui + 1) * (Du + fma(dQ, (R)l, dP)) * (R)0.5;
+}
+
+// Segment k >= 1 of row p (pool), as integers.
+template <typename R>
+struct Seg { int u, v; R a, s; };
+
+template <typename R>
+__device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, int k, int c, int Mx)
+{
+    Seg<R> sg;
+    if (k == 0) {
+        sg.u = 1; sg.v = (int)rw.lv[p]; sg.a = rw.la[p]; sg.s = rw.ls[p];
+    } else {
+        const long long q = rw.off[p] + k - 1;
+        sg.u = pl.u[q]; sg.a = pl.a[q]; sg.s = pl.s[q];
+        sg.v = (k + 1 < c) ? pl.u[q + 1] - 1 : Mx;
+    }
+    return sg;
 }
 
 // sum_{m=m0}^{m1} max(P + Q m, env_p(m)), one step at a time (eq:t_ij1 as
@@ -304,10 +323,11 @@ struct Smem {
     int* I;        // [K] original lengths
     int* Is;       // [K] sorted lengths
     int* ord;      // [K] sorted pos -> task
+    short* jlo;    // [K] first feasible j of row i (memory window), > i if none
     short* S;      // [ng][K] boundaries (1-based j*)
     double* tinf;  // [ng]
     double* red;   // [2 * kWarps]
-    int* ctl;      // [0] gamma queue, [1] overflow flag, [2] scenario status, [3] bad flag
+    int* ctl;      // [0] gamma queue, [2] M, [3] bad flag
     long long* sid;
     unsigned char* rows; // [kWarps] row states when rows_in_smem
 };
@@ -317,7 +337,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
-    b += (size_t)ng * K * sizeof(short);
+    b += (size_t)(ng + 1) * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
@@ -332,6 +352,7 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     s.I = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.Is = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.ord = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
+    s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.S = reinterpret_cast<short*>(base + b); b += (size_t)ng * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
@@ -343,38 +364,122 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     return s;
 }
 
+// ------------------------------------------------------------ envelope update
+// Row i's Upsilon1 for n >= 2 (eq:tt2):  env_i(m) = max(P + Q m, env_p(m)) + Av + Bv m.
+// The set where the new line beats the convex env_p is one interval [mlo, mhi].
+// Executed by the single lane that owns j*; returns true on pool overflow.
+template <typename R>
+__device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R P, R Q, R Av, R Bv,
+                           int Mx, long long& top)
+{
+    const int cntp = rw.cnt[p];
+    const long long base = top;
+    rw.off[i] = (int)base;
+    if (cntp == 0) { rw.cnt[i] = 0; return false; }            // N = 1: no n >= 2 steps
+    if (cntp == 1) {                                           // fast path: one old line on [1, Mx]
+        const R ea = rw.la[p], es = rw.ls[p];
+        const R dP = P - ea, dQ = Q - es;
+        const R Du = dP + dQ, Dv = fma(dQ, (R)Mx, dP);
+        if (!(Du > (R)0) && !(Dv > (R)0)) {                    // old line everywhere
+            rw.la[i] = ea + Av; rw.ls[i] = es + Bv; rw.lv[i] = (R)Mx; rw.cnt[i] = 1;
+            return false;
+        }
+        if (Du > (R)0 && Dv > (R)0) {                          // new line everywhere
+            rw.la[i] = P + Av; rw.ls[i] = Q + Bv; rw.lv[i] = (R)Mx; rw.cnt[i] = 1;
+            return false;
+        }
+        if (base >= pl.cap) return true;
+        if (Dv > (R)0) {                                       // old on [1, f-1], new on [f, Mx]
+            const int f = first_pos(dP, dQ, 1, Mx);
+            rw.la[i] = ea + Av; rw.ls[i] = es + Bv; rw.lv[i] = (R)(f - 1);
+            pl.u[base] = f; pl.a[base] = P + Av; pl.s[base] = Q + Bv;
+        } else {                                               // new on [1, l], old on [l+1, Mx]
+            const int l = last_pos(dP, dQ, 1, Mx);
+            rw.la[i] = P + Av; rw.ls[i] = Q + Bv; rw.lv[i] = (R)l;
+            pl.u[base] = l + 1; pl.a[base] = ea + Av; pl.s[base] = es + Bv;
+        }
+        rw.cnt[i] = 2;
+        top = base + 1;
+        return false;
+    }
+    int mlo = 0, mhi = -1;
+    for (int k = 0; k < cntp && mlo == 0; ++k) {
+        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+        const R dP = P - sg.a, dQ = Q - sg.s;
+        if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0) mlo = first_pos(dP, dQ, sg.u, sg.v);
+    }
+    if (mlo > 0)
+        for (int k = cntp - 1; k >= 0; --k) {
+            const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+            const R dP = P - sg.a, dQ = Q - sg.s;
+            if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0) {
+                mhi = last_pos(dP, dQ, sg.u, sg.v);
+                break;
+            }
+        }
+    int nseg = 0;
+    bool ovf = false;
+    rw.lv[i] = (R)Mx;
+    auto emit = [&](int u, R a, R s) {
+        a += Av;
+        s += Bv;
+        if (nseg == 0) { rw.la[i] = a; rw.ls[i] = s; }
+        else {
+            if (nseg == 1) rw.lv[i] = (R)(u - 1);
+            const long long q = base + nseg - 1;
+            if (q >= pl.cap) ovf = true;
+            else { pl.u[q] = u; pl.a[q] = a; pl.s[q] = s; }
+        }
+        ++nseg;
+    };
+    bool line_done = false;
+    for (int k = 0; k < cntp; ++k) {
+        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+        if (mlo > 0 && sg.v >= mlo && sg.u <= mhi) {
+            if (sg.u < mlo) emit(sg.u, sg.a, sg.s);            // left remainder
+            if (!line_done) { emit(mlo, P, Q); line_done = true; }
+            if (sg.v > mhi) emit(mhi + 1, sg.a, sg.s);         // right remainder
+        } else {
+            emit(sg.u, sg.a, sg.s);
+        }
+    }
+    rw.cnt[i] = nseg;
+    top = base + (nseg > 1 ? nseg - 1 : 0);
+    return ovf;
+}
+
 // ------------------------------------------------------------ the DP of one gamma
 // Returns T_inf (= Upsilon[K,0,0]) or +inf if some row has no feasible batch;
 // sets *overflow if the segment pool ran out.  S[i-1] = j* (1-based).
 template <typename R, int ALGO>
 __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> pl, int gamma,
                            double alpha, double c1d, double c2d, double c1v, double c2v,
-                           short* S, bool* overflow)
+                           short* S, bool* overflow, WorkCount& wc)
 {
     const int lane = threadIdx.x & 31;
     const int K = C.K;
     const double L = expected_tokens(alpha, gamma);
     const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
     const int Mx = N - 1;                                        // n >= 2 <-> m = n-1 in [1, Mx]
+    const R Mxr = (R)Mx;
     const R sumM = (R)((double)Mx * (double)(Mx + 1) * 0.5);
     long long top = 0;                                           // pool bump pointer
+    unsigned n_cand = 0, n_seg = 0;
 
     if (lane == 0) {                                             // row 0 == 0 (reading A3)
         rw.y0[0] = rw.y1[0] = rw.a0[0] = rw.s0[0] = rw.es[0] = (R)0;
         rw.la[0] = rw.ls[0] = (R)0;
+        rw.lv[0] = Mxr;
         rw.off[0] = 0;
         rw.cnt[0] = Mx >= 1 ? 1 : 0;
     }
     __syncwarp();
 
-    const long long room = C.gamma_s - C.Gp;
     double T_last = 0.0;
-    int row_ovf = 0;
+    int rows_done = 0;
     for (int i = 1; i <= K; ++i) {
         const int I = sm.Is[i - 1];
-        // memory window (Alg. 1 lines 10-13): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
-        long long bmax = room >= 0 ? room / (C.kvunit * ((long long)I + C.O_max)) : 0;
-        const int jlo = bmax >= i ? 1 : (int)(i - bmax + 1);
+        const int jlo = sm.jlo[i - 1];       // memory window (Alg. 1 lines 10-13)
         if (jlo > i) { T_last = dinf(); break; }
         const RowCoef rc = row_coef(C, c1d, c2d, c1v, c2v, gamma, L, I);
 
@@ -387,18 +492,23 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
             for (int j = jlo + lane; j <= i; j += 32) {
                 const int p = j - 1, b = i - j + 1;
                 const Cand<R> c = cand_terms(rw, rc, p, b);
-                R acc;
                 const int cntp = rw.cnt[p];
+                R acc;
                 if (ALGO == SDEDGE_ALGO_ENVELOPE) {
                     acc = rw.es[p];
-                    for (int k = 0; k < cntp; ++k) {
-                        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
-                        acc += pos_sum(c.P - sg.a, c.Q - sg.s, sg.u, sg.v);
+                    if (cntp > 0) {
+                        acc += pos_sum(c.P - rw.la[p], c.Q - rw.ls[p], (R)1, rw.lv[p]);
+                        for (int k = 1; k < cntp; ++k) {
+                            const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+                            acc += pos_sum(c.P - sg.a, c.Q - sg.s, (R)sg.u, (R)sg.v);
+                        }
                     }
                 } else {
                     acc = dense_sum(rw, pl, p, c.P, c.Q, 1, Mx, Mx);
                 }
-                const R rest = acc + fma(c.Bv, sumM, (R)Mx * c.Av);
+                n_cand += 1;
+                n_seg += (unsigned)cntp;
+                const R rest = acc + fma(c.Bv, sumM, Mxr * c.Av);
                 const R T = c.d1 + rest;
                 if (T <= bT) { bT = T; bj = j; brest = rest; }   // '>=' of Alg. 1 line 21
             }
@@ -416,31 +526,24 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
                 c = cand_terms(rw, rc, p, b);
                 const int chunk = (Mx + gsz - 1) / gsz;
                 const int m0 = 1 + sub * chunk, m1 = min(Mx, m0 + chunk - 1);
-                const R acc = dense_sum(rw, pl, p, c.P, c.Q, m0, m1, Mx);
-                rest = acc;
+                rest = dense_sum(rw, pl, p, c.P, c.Q, m0, m1, Mx);
             }
             for (int o = gsz >> 1; o > 0; o >>= 1) rest += __shfl_xor_sync(0xffffffffu, rest, o);
             if (ci < nc && sub == 0) {
-                rest = rest + fma(c.Bv, sumM, (R)Mx * c.Av);
+                n_cand += 1;
+                n_seg += (unsigned)rw.cnt[j - 1];
+                rest = rest + fma(c.Bv, sumM, Mxr * c.Av);
                 bT = c.d1 + rest;
                 bj = j;
                 brest = rest;
             }
         }
-        // warp argmin over (T, j): smaller T, then larger j (reading A6)
-        R t = bT;
-        int jj = bj;
-        for (int o = 16; o > 0; o >>= 1) {
-            const R ot = __shfl_xor_sync(0xffffffffu, t, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, jj, o);
-            if (ot < t || (ot == t && oj > jj)) { t = ot; jj = oj; }
-        }
-        if (jj < 0) { T_last = dinf(); break; }               // no finite candidate
-        const unsigned own = __ballot_sync(0xffffffffu, bj == jj);
-        const int src = __ffs(own) - 1;
-        const R rest_star = __shfl_sync(0xffffffffu, brest, src);
-
-        if (lane == 0) {
+        R tmin;
+        const int jj = warp_argmin(bT, bj, &tmin);
+        if (jj < 0) { T_last = dinf(); break; }                // no finite candidate
+        const int owner = __ffs(__ballot_sync(0xffffffffu, bj == jj)) - 1;
+        int ovf = 0;
+        if (lane == owner) {
             // eq:rg, eq:tt1, eq:tt2 with j* (reading A4: S[i] always set)
             S[i - 1] = (short)jj;
             const int p = jj - 1, b = i - jj + 1;
@@ -449,69 +552,32 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
             rw.y1[i] = c.d1;
             rw.a0[i] = c.P;
             rw.s0[i] = c.Q;
-            rw.es[i] = rest_star;
-            // env_i(m) = max(P + Q m, env_p(m)) + Av + Bv m.  The positive set of
-            // (line - env_p) is one interval [mlo, mhi] (env_p convex).
-            const int cntp = rw.cnt[p];
-            int mlo = 0, mhi = -1;
-            for (int k = 0; k < cntp && mlo == 0; ++k) {
-                const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
-                const R dP = c.P - sg.a, dQ = c.Q - sg.s;
-                if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0)
-                    mlo = first_pos(dP, dQ, sg.u, sg.v);
-            }
-            if (mlo > 0)
-                for (int k = cntp - 1; k >= 0; --k) {
-                    const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
-                    const R dP = c.P - sg.a, dQ = c.Q - sg.s;
-                    if (fma(dQ, (R)sg.u, dP) > (R)0 || fma(dQ, (R)sg.v, dP) > (R)0) {
-                        mhi = last_pos(dP, dQ, sg.u, sg.v);
-                        break;
-                    }
-                }
-            int nseg = 0;
-            const long long base = top;
-            bool ovf = false;
-            auto emit = [&](int u, R a, R s) {
-                a += c.Av;
-                s += c.Bv;
-                if (nseg == 0) { rw.la[i] = a; rw.ls[i] = s; }
-                else {
-                    const long long q = base + nseg - 1;
-                    if (q >= pl.cap) { ovf = true; }
-                    else { pl.u[q] = u; pl.a[q] = a; pl.s[q] = s; }
-                }
-                ++nseg;
-            };
-            bool line_done = false;
-            for (int k = 0; k < cntp; ++k) {
-                const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
-                if (mlo > 0 && sg.v >= mlo && sg.u <= mhi) {
-                    if (sg.u < mlo) emit(sg.u, sg.a, sg.s);          // left remainder
-                    if (!line_done) { emit(mlo, c.P, c.Q); line_done = true; }
-                    if (sg.v > mhi) emit(mhi + 1, sg.a, sg.s);       // right remainder
-                } else {
-                    emit(sg.u, sg.a, sg.s);
-                }
-            }
-            rw.off[i] = (int)base;
-            rw.cnt[i] = nseg;
-            top = base + (nseg > 1 ? nseg - 1 : 0);
-            row_ovf = ovf;
+            rw.es[i] = brest;
+            ovf = env_update(rw, pl, p, i, c.P, c.Q, c.Av, c.Bv, Mx, top) ? 1 : 0;
         }
-        top = __shfl_sync(0xffffffffu, top, 0);
-        row_ovf = __shfl_sync(0xffffffffu, row_ovf, 0);
+        top = __shfl_sync(0xffffffffu, top, owner);
+        ovf = __shfl_sync(0xffffffffu, ovf, owner);
         __syncwarp();
-        if (row_ovf) { *overflow = true; T_last = dinf(); break; }
-        T_last = (double)t;
+        ++rows_done;
+        if (ovf) { *overflow = true; T_last = dinf(); break; }
+        T_last = (double)tmin;
     }
+    wc.cand += n_cand;
+    wc.seg += n_seg;
+    wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
+    if (lane == 0) wc.rows += rows_done;
     return T_last;
 }
 
+
 // ------------------------------------------------------------ the fused kernel
-template <typename R, int ALGO, int BIG>
-__global__ void __launch_bounds__(kThreads)
-solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws)
+#ifndef SDEDGE_MINB
+#define SDEDGE_MINB 4     // min resident CTAs per SM requested from ptxas (128-register cap)
+#endif
+
+template <typename R, int ALGO, int RSMEM>
+__global__ void __launch_bounds__(kThreads, SDEDGE_MINB)
+solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws, int BIG)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = C.K, ng = C.ng;
@@ -519,11 +585,16 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long slot = (long long)blockIdx.x * kWarps + warp;
 
-    Rows<R> rw = carve_rows<R>(C.rows_in_smem ? sm.rows + (size_t)warp * rows_bytes<R>(K)
-                                              : ws.rows + (size_t)slot * C.rows_stride, K);
+    // RSMEM is a template parameter so that the compiler sees shared-window
+    // (32-bit, LDS/STS) addresses for the row state instead of generic ones.
+    Rows<R> rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)warp * rows_bytes<R>(K)
+                                     : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     __shared__ bool s_ovf;
+    __shared__ unsigned long long s_work[4];
+    if (tid < 4) s_work[tid] = 0;
+    WorkCount wc;
 
     for (;;) {
         if (tid == 0) {
@@ -559,6 +630,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             sm.ord[r] = k;
             sm.Is[r] = Ik;
         }
+        __syncthreads();
+        // ---- memory window per sorted row (gamma-independent): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
+        for (int r = tid; r < K; r += kThreads) {
+            const long long room = C.gamma_s - C.Gp;
+            const long long bmax = room >= 0 ? room / (C.kvunit * ((long long)sm.Is[r] + C.O_max)) : 0;
+            const int i = r + 1;
+            sm.jlo[r] = (short)(bmax >= i ? 1 : (int)(i - bmax + 1));
+        }
         // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2)
         double tc = 0.0, q = 0.0;
         if (!bad)
@@ -593,7 +672,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 if (gi >= ng) break;
                 bool ovf = false;
                 const double t = dp_gamma<R, ALGO>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
-                                                   sm.S + (size_t)gi * K, &ovf);
+                                                   sm.S + (size_t)gi * K, &ovf, wc);
                 if (lane == 0) {
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
@@ -659,6 +738,15 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 out.w[s * K + k] = wk;
             }
         __syncthreads();
+    }
+    if (out.work) {
+        unsigned long long v[4] = {wc.cand, wc.seg, wc.steps, wc.rows};
+        for (int q = 0; q < 4; ++q) {
+            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+            if (lane == 0) atomicAdd(&s_work[q], v[q]);
+        }
+        __syncthreads();
+        if (tid < 4) atomicAdd(out.work + tid, s_work[tid]);
     }
 }
 
@@ -739,8 +827,8 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
-    auto k_main = solve_kernel<R, ALGO, 0>;
-    auto k_big = solve_kernel<R, ALGO, 1>;
+    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1> : solve_kernel<R, ALGO, 0>;
+    auto k_big = k_main;
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     int occ = 0;
@@ -779,12 +867,12 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (n > 0) {
         C.pool_cap = cap_main;
         w.pool = wsb + o_pool;
-        k_main<<<(unsigned)grid, kThreads, sb, st>>>(C, in, out, n, w);
+        k_main<<<(unsigned)grid, kThreads, sb, st>>>(C, in, out, n, w, 0);
         ++launches;
         CU(cudaGetLastError());
         C.pool_cap = cap_big;
         w.pool = wsb + o_pool_big;
-        k_big<<<(unsigned)grid_big, kThreads, sb, st>>>(C, in, out, n, w);
+        k_big<<<(unsigned)grid_big, kThreads, sb, st>>>(C, in, out, n, w, 1);
         ++launches;
         CU(cudaGetLastError());
     }
@@ -808,7 +896,8 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     C.Gp = (long long)C.Jd * (8LL * C.hd * C.hd + 4LL * C.hd * C.h2d);                      // eq:memory_model
     C.kvunit = 4LL * C.Jd * C.hd;                                                            // eq:memory_kv
     Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
-    Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status};
+    Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
+                reinterpret_cast<unsigned long long*>(o->work_counters)};
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
     if (p->precision == 0)
         return p->algo == SDEDGE_ALGO_DENSE ? launch_all<double, SDEDGE_ALGO_DENSE>(C, in, out, n, st, p->flags)
@@ -867,7 +956,8 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
                         bC ? reinterpret_cast<double*>(d + oC) : nullptr};
     sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm), reinterpret_cast<int32_t*>(d + oM),
                          reinterpret_cast<int32_t*>(d + oBe), reinterpret_cast<int32_t*>(d + oOr),
-                         bW ? reinterpret_cast<double*>(d + oW) : nullptr, reinterpret_cast<int32_t*>(d + oSt)};
+                         bW ? reinterpret_cast<double*>(d + oW) : nullptr, reinterpret_cast<int32_t*>(d + oSt),
+                         nullptr};
     rc = solve_device(&ds, n, p, reinterpret_cast<double*>(d + oLat), &dsch);
     if (rc) return rc;
     CU(cudaMemcpyAsync(out_latency, d + oLat, bLat, cudaMemcpyDeviceToHost, st));

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layout_matches_header():
     # sdedge_params: 2 models (24 B) + 4 c + B_w + sigma + lambda (56) + int64 + 7 int32 + pad + double + ptr
     assert C.sizeof(sd.SdedgeParams) == 136
-    assert C.sizeof(sd.SdedgeScenarios) == 40 and C.sizeof(sd.SdedgeSchedule) == 48
+    assert C.sizeof(sd.SdedgeScenarios) == 40 and C.sizeof(sd.SdedgeSchedule) == 56
 
 
 @pytest.mark.parametrize("bad", [dict(K=0), dict(K=1025), dict(gamma_min=3, gamma_max=2),
@@ -44,7 +44,7 @@ def test_invalid_arguments_rejected_without_gpu(bad):
     pd = dict(scengen.params("68M-7B", K=4), **bad)
     P = sd.make_params(pd)
     sc = sd.SdedgeScenarios(1, 1, 1, 1, None)
-    sch = sd.SdedgeSchedule(1, 1, 1, 1, None, 1)
+    sch = sd.SdedgeSchedule(1, 1, 1, 1, None, 1, None)
     rc = sd.lib().sdedge_solve_batch(C.byref(sc), 1, C.byref(P), 1, C.byref(sch))
     assert rc == -1 and sd.sdedge_last_error()
 
@@ -52,7 +52,7 @@ def test_invalid_arguments_rejected_without_gpu(bad):
 def test_null_pointers_rejected():
     P = sd.make_params(scengen.params("68M-7B", K=4))
     sc = sd.SdedgeScenarios(None, 1, 1, 1, None)
-    sch = sd.SdedgeSchedule(1, 1, 1, 1, None, 1)
+    sch = sd.SdedgeSchedule(1, 1, 1, 1, None, 1, None)
     assert sd.lib().sdedge_solve_batch(C.byref(sc), 1, C.byref(P), 1, C.byref(sch)) == -1
     assert sd.lib().sdedge_solve_batch(None, 1, C.byref(P), 1, C.byref(sch)) == -1
     assert sd.lib().sdedge_solve_batch(C.byref(sc), -1, C.byref(P), 1, C.byref(sch)) == -1
