@@ -66,6 +66,21 @@ def parse():
     return ap.parse_args()
 
 
+def shard(rank: int, n_per_rank: int):
+    """Weak scaling: rank r owns scenarios [r n, (r+1) n) of the counter-based stream."""
+    return rank * n_per_rank, (rank + 1) * n_per_rank
+
+
+def max_over_ranks(x: float, dist, device) -> float:
+    """Max of a per-rank time over all ranks (the multi-GPU timing rule)."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,7 +216,7 @@ def main():
 
     pd, _, n_total = scengen.config(args.config, 0, 1, pair=args.pair)
     n = args.n or n_total
-    s0 = rank * n                                           # weak scaling: own shard per rank
+    s0, _ = shard(rank, n)                                  # weak scaling: own shard per rank
     t_gen = time.perf_counter()
     _, sc, _ = scengen.config(args.config, s0, s0 + n, pair=args.pair)
     t_gen = time.perf_counter() - t_gen
@@ -244,11 +259,7 @@ def main():
         if ws > 1:
             dist.barrier()
     el = e0.elapsed_time(e1) * 1e-3
-    el_max = el
-    if ws > 1:
-        t = torch.tensor([el], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el_max = float(t.item())
+    el_max = max_over_ranks(el, dist, dev)
     wk = work.cpu().numpy().astype(np.float64) / args.steps    # per step (= per main launch)
     status_ok = int((out["status"] == 0).sum().item())
 
@@ -271,11 +282,7 @@ def main():
                           precision=prec, algo=algo)
         f1.record(stream)
         torch.cuda.synchronize()
-        te = max(f0.elapsed_time(f1) * 1e-3, 0.0)
-        if ws > 1:
-            t = torch.tensor([te], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+        te = max_over_ranks(f0.elapsed_time(f1) * 1e-3, dist, dev)
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         d2h = sum(v.numel() * v.element_size() for v in hout.values() if v is not None)
         e2e = {"value": n * ws * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d,

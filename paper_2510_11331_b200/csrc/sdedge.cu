@@ -87,31 +87,36 @@ struct Work {
     unsigned char* pool;           // envelope segment pools, one per warp slot
 };
 
-// DP row state of one warp (SoA, generic pointers: smem or global).
+// DP row state of one warp (SoA of pairs, generic pointers: smem or global).
+template <typename R> struct Pair;
+template <> struct Pair<double> { using T = double2; };
+template <> struct Pair<float> { using T = float2; };
+template <typename R> using R2 = typename Pair<R>::T;
+
 template <typename R>
 struct Rows {
-    R *y0, *y1;        // Upsilon[p, 1, 0], Upsilon[p, 1, 1]
-    R *a0, *s0;        // Upsilon[p, n, 0] = a0 + s0 (n-1), n >= 2
-    R *es;             // sum_{n=2}^{N} Upsilon[p, n, 1]
-    R *la, *ls, *lv;   // first envelope segment: line (intercept, slope in m = n-1), last m
+    R2<R>* Y;          // (Upsilon[p,1,0], Upsilon[p,1,1])
+    R2<R>* A;          // Upsilon[p,n,0] = A.x + A.y (n-1), n >= 2
+    R2<R>* E;          // (sum_{n=2}^{N} Upsilon[p,n,1], last m of the first envelope segment)
+    R2<R>* Ln;         // first envelope segment's line (intercept, slope in m = n-1)
     int *off, *cnt;    // extra segments pool[off .. off+cnt-2]; cnt = #segments
 };
 
 template <typename R>
 __host__ __device__ inline size_t rows_bytes(int K)
 {
-    return (size_t)(K + 1) * (8 * sizeof(R) + 2 * sizeof(int));
+    // rounded to 16 B so that every warp's pair arrays stay 16-byte aligned (LDS.128)
+    return ((size_t)(K + 1) * (8 * sizeof(R) + 2 * sizeof(int)) + 15) & ~(size_t)15;
 }
 
 template <typename R>
 __device__ inline Rows<R> carve_rows(unsigned char* base, int K)
 {
     Rows<R> r;
-    size_t n = (size_t)K + 1;
-    R* f = reinterpret_cast<R*>(base);
-    r.y0 = f; r.y1 = f + n; r.a0 = f + 2 * n; r.s0 = f + 3 * n; r.es = f + 4 * n;
-    r.la = f + 5 * n; r.ls = f + 6 * n; r.lv = f + 7 * n;
-    int* q = reinterpret_cast<int*>(f + 8 * n);
+    const size_t n = (size_t)K + 1;
+    R2<R>* f = reinterpret_cast<R2<R>*>(base);
+    r.Y = f; r.A = f + n; r.E = f + 2 * n; r.Ln = f + 3 * n;
+    int* q = reinterpret_cast<int*>(f + 4 * n);
     r.off = q; r.cnt = q + n;
     return r;
 }
@@ -224,7 +229,8 @@ __device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, in
 {
     Seg<R> sg;
     if (k == 0) {
-        sg.u = 1; sg.v = (int)rw.lv[p]; sg.a = rw.la[p]; sg.s = rw.ls[p];
+        const R2<R> ln = rw.Ln[p];
+        sg.u = 1; sg.v = (int)rw.E[p].y; sg.a = ln.x; sg.s = ln.y;
     } else {
         const long long q = rw.off[p] + k - 1;
         sg.u = pl.u[q]; sg.a = pl.a[q]; sg.s = pl.s[q];
@@ -254,58 +260,57 @@ __device__ inline R dense_sum(const Rows<R>& rw, const Pool<R>& pl, int p, R P, 
     return acc;
 }
 
-// Warp-uniform per-row stage-time coefficients (per unit batch size b) for
-// sorted position i with padded length I: Appendix-A closed forms of
-// eq:d_latency / eq:v_latency summed over the draft passes (D1).
-struct RowCoef {
-    double td1, ad, bd;   // draft: n = 1 value, n >= 2 intercept, slope  (x b)
-    double tv1, av, bv;   // verify (x b)
-    double c2dg, c2vv;    // gamma c2d, c2v + downlink  (not x b)
+// Stage-time coefficients (D1: Appendix-A closed forms of eq:d_latency /
+// eq:v_latency summed over the gamma draft passes; everything per unit batch size b).
+// Per (scenario, gamma): the I-independent parts.
+struct DPConst {
+    double kd, kv;        // c1d 4 Jd hd,  c1v 4 Jv hv
+    double hd2, hv2;      // 2 hd + h2d,   2 hv + h2v
+    double g, tri;        // gamma, gamma (gamma-1) / 2
+    double bdc, bvc;      // draft / verify slopes in n:  kd gamma L,  kv (1+gamma) L
+    double c2dg, c2vv;    // gamma c2d,  c2v + downlink
+    double sumM, Mx;      // sum_{m=1}^{N-1} m,  N - 1
 };
 
-__device__ inline RowCoef row_coef(const Consts& C, double c1d, double c2d, double c1v, double c2v,
-                                   int gamma, double L, int I)
+// Per sorted row i with padded length I.
+struct RowCoef {
+    double td1, ad;       // draft: n = 1 value, n >= 2 intercept            (x b, + c2dg)
+    double tv1, av;       // verify: n = 1 value, n >= 2 intercept           (x b, + c2vv)
+    double tvb, tvc;      // sum_{n>=2} T^v_n = b tvb + tvc  (closed form, hoisted)
+};
+
+__device__ inline RowCoef row_coef(const DPConst& D, int I)
 {
     RowCoef r;
-    const double g = gamma, Id = I;
-    const double kd = c1d * (4.0 * C.Jd * (double)C.hd);
-    const double kv = c1v * (4.0 * C.Jv * (double)C.hv);
-    const double hd2 = 2.0 * C.hd + C.h2d, hv2 = 2.0 * C.hv + C.h2v;
-    if (gamma > 0) {
-        const double tri = g * (g - 1.0) * 0.5;               // sum_{i=1}^{g} (i-1)
-        r.td1 = kd * (Id * (hd2 + Id) + (g - 1.0) * (hd2 + Id) + tri);
-        r.ad = kd * (g * (hd2 + Id) + tri);
-        r.bd = kd * g * L;
+    const double Id = I;
+    const double hI = D.hd2 + Id;
+    if (D.g > 0.0) {
+        r.td1 = D.kd * ((Id + D.g - 1.0) * hI + D.tri);      // prefill pass + (gamma-1) decode passes at n = 1
+        r.ad = D.kd * (D.g * hI + D.tri);
     } else {
-        r.td1 = r.ad = r.bd = 0.0;                            // gamma = 0: no draft passes
+        r.td1 = r.ad = 0.0;                                  // gamma = 0: no draft passes
     }
-    r.tv1 = kv * (Id + g) * (hv2 + Id + g);
-    r.av = kv * (1.0 + g) * (hv2 + Id + g);
-    r.bv = kv * (1.0 + g) * L;
-    r.c2dg = g * c2d;
-    r.c2vv = c2v + C.dl;
+    const double vI = D.hv2 + Id + D.g;
+    r.tv1 = D.kv * (Id + D.g) * vI;
+    r.av = D.kv * (1.0 + D.g) * vI;
+    r.tvb = fma(D.bvc, D.sumM, r.av * D.Mx);
+    r.tvc = D.c2vv * D.Mx;
     return r;
 }
 
-// Candidate data of (i, j) with b = i - j + 1 for predecessor row p = j - 1.
+// Candidate data of (i, j) with batch size b (as a double) for predecessor row p = j - 1.
 template <typename R>
-struct Cand { R d0, d1, P, Q, Av, Bv; };
+struct Cand { R d0, d1, P, Q; };
 
 template <typename R>
-__device__ inline Cand<R> cand_terms(const Rows<R>& rw, const RowCoef& rc, int p, int b)
+__device__ inline Cand<R> cand_terms(const Rows<R>& rw, const DPConst& D, const RowCoef& rc, int p, double bd)
 {
-    const double bd = b;
     Cand<R> c;
-    const R Td1 = (R)fma(bd, rc.td1, rc.c2dg);
-    const R Tv1 = (R)fma(bd, rc.tv1, rc.c2vv);
-    const R Ad = (R)fma(bd, rc.ad, rc.c2dg);
-    const R Bd = (R)(bd * rc.bd);
-    c.Av = (R)fma(bd, rc.av, rc.c2vv);
-    c.Bv = (R)(bd * rc.bv);
-    c.d0 = rw.y0[p] + Td1;                       // eq:tt1 at n = 1
-    c.d1 = rmax(c.d0, rw.y1[p]) + Tv1;           // eq:tt2 at n = 1 (reading A1)
-    c.P = rw.a0[p] + Ad;                         // Upsilon0 line of the candidate, n >= 2
-    c.Q = rw.s0[p] + Bd;
+    const R2<R> y = rw.Y[p], a = rw.A[p];
+    c.d0 = y.x + (R)fma(bd, rc.td1, D.c2dg);             // eq:tt1 at n = 1
+    c.d1 = rmax(c.d0, y.y) + (R)fma(bd, rc.tv1, D.c2vv);  // eq:tt2 at n = 1 (reading A1)
+    c.P = a.x + (R)fma(bd, rc.ad, D.c2dg);               // Upsilon0 line of the candidate, n >= 2
+    c.Q = a.y + (R)(bd * D.bdc);
     return c;
 }
 
@@ -377,25 +382,26 @@ __device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R
     rw.off[i] = (int)base;
     if (cntp == 0) { rw.cnt[i] = 0; return false; }            // N = 1: no n >= 2 steps
     if (cntp == 1) {                                           // fast path: one old line on [1, Mx]
-        const R ea = rw.la[p], es = rw.ls[p];
+        const R2<R> ln = rw.Ln[p];
+        const R ea = ln.x, es = ln.y;
         const R dP = P - ea, dQ = Q - es;
         const R Du = dP + dQ, Dv = fma(dQ, (R)Mx, dP);
         if (!(Du > (R)0) && !(Dv > (R)0)) {                    // old line everywhere
-            rw.la[i] = ea + Av; rw.ls[i] = es + Bv; rw.lv[i] = (R)Mx; rw.cnt[i] = 1;
+            rw.Ln[i] = R2<R>{ea + Av, es + Bv}; rw.E[i].y = (R)Mx; rw.cnt[i] = 1;
             return false;
         }
         if (Du > (R)0 && Dv > (R)0) {                          // new line everywhere
-            rw.la[i] = P + Av; rw.ls[i] = Q + Bv; rw.lv[i] = (R)Mx; rw.cnt[i] = 1;
+            rw.Ln[i] = R2<R>{P + Av, Q + Bv}; rw.E[i].y = (R)Mx; rw.cnt[i] = 1;
             return false;
         }
         if (base >= pl.cap) return true;
         if (Dv > (R)0) {                                       // old on [1, f-1], new on [f, Mx]
             const int f = first_pos(dP, dQ, 1, Mx);
-            rw.la[i] = ea + Av; rw.ls[i] = es + Bv; rw.lv[i] = (R)(f - 1);
+            rw.Ln[i] = R2<R>{ea + Av, es + Bv}; rw.E[i].y = (R)(f - 1);
             pl.u[base] = f; pl.a[base] = P + Av; pl.s[base] = Q + Bv;
         } else {                                               // new on [1, l], old on [l+1, Mx]
             const int l = last_pos(dP, dQ, 1, Mx);
-            rw.la[i] = P + Av; rw.ls[i] = Q + Bv; rw.lv[i] = (R)l;
+            rw.Ln[i] = R2<R>{P + Av, Q + Bv}; rw.E[i].y = (R)l;
             pl.u[base] = l + 1; pl.a[base] = ea + Av; pl.s[base] = es + Bv;
         }
         rw.cnt[i] = 2;
@@ -419,13 +425,13 @@ __device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R
         }
     int nseg = 0;
     bool ovf = false;
-    rw.lv[i] = (R)Mx;
+    rw.E[i].y = (R)Mx;
     auto emit = [&](int u, R a, R s) {
         a += Av;
         s += Bv;
-        if (nseg == 0) { rw.la[i] = a; rw.ls[i] = s; }
+        if (nseg == 0) { rw.Ln[i] = R2<R>{a, s}; }
         else {
-            if (nseg == 1) rw.lv[i] = (R)(u - 1);
+            if (nseg == 1) rw.E[i].y = (R)(u - 1);
             const long long q = base + nseg - 1;
             if (q >= pl.cap) ovf = true;
             else { pl.u[q] = u; pl.a[q] = a; pl.s[q] = s; }
@@ -461,15 +467,27 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
     const double L = expected_tokens(alpha, gamma);
     const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
     const int Mx = N - 1;                                        // n >= 2 <-> m = n-1 in [1, Mx]
-    const R Mxr = (R)Mx;
-    const R sumM = (R)((double)Mx * (double)(Mx + 1) * 0.5);
+    DPConst D;
+    D.g = gamma;
+    D.tri = D.g * (D.g - 1.0) * 0.5;                             // sum_{i=1}^{gamma} (i-1)
+    D.kd = c1d * (4.0 * C.Jd * (double)C.hd);
+    D.kv = c1v * (4.0 * C.Jv * (double)C.hv);
+    D.hd2 = 2.0 * C.hd + C.h2d;
+    D.hv2 = 2.0 * C.hv + C.h2v;
+    D.bdc = D.kd * D.g * L;
+    D.bvc = D.kv * (1.0 + D.g) * L;
+    D.c2dg = D.g * c2d;
+    D.c2vv = c2v + C.dl;
+    D.Mx = Mx;
+    D.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
     long long top = 0;                                           // pool bump pointer
     unsigned n_cand = 0, n_seg = 0;
 
     if (lane == 0) {                                             // row 0 == 0 (reading A3)
-        rw.y0[0] = rw.y1[0] = rw.a0[0] = rw.s0[0] = rw.es[0] = (R)0;
-        rw.la[0] = rw.ls[0] = (R)0;
-        rw.lv[0] = Mxr;
+        rw.Y[0] = R2<R>{(R)0, (R)0};
+        rw.A[0] = R2<R>{(R)0, (R)0};
+        rw.E[0] = R2<R>{(R)0, (R)Mx};
+        rw.Ln[0] = R2<R>{(R)0, (R)0};
         rw.off[0] = 0;
         rw.cnt[0] = Mx >= 1 ? 1 : 0;
     }
@@ -478,26 +496,28 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
     double T_last = 0.0;
     int rows_done = 0;
     for (int i = 1; i <= K; ++i) {
-        const int I = sm.Is[i - 1];
         const int jlo = sm.jlo[i - 1];       // memory window (Alg. 1 lines 10-13)
         if (jlo > i) { T_last = dinf(); break; }
-        const RowCoef rc = row_coef(C, c1d, c2d, c1v, c2v, gamma, L, I);
+        const RowCoef rc = row_coef(D, sm.Is[i - 1]);
 
         R bT = kinf<R>();
         int bj = -1;
         R brest = (R)0;
         const int nc = i - jlo + 1;
         if (ALGO == SDEDGE_ALGO_ENVELOPE || nc >= 17) {
-            // one lane per candidate, ascending j per lane
-            for (int j = jlo + lane; j <= i; j += 32) {
-                const int p = j - 1, b = i - j + 1;
-                const Cand<R> c = cand_terms(rw, rc, p, b);
+            // one lane per candidate, ascending j per lane (so '<=' keeps the largest j)
+            double bd = (double)(i - jlo - lane + 1);
+            for (int j = jlo + lane; j <= i; j += 32, bd -= 32.0) {
+                const int p = j - 1;
+                const Cand<R> c = cand_terms(rw, D, rc, p, bd);
                 const int cntp = rw.cnt[p];
                 R acc;
                 if (ALGO == SDEDGE_ALGO_ENVELOPE) {
-                    acc = rw.es[p];
+                    const R2<R> e = rw.E[p];
+                    acc = e.x;                                   // sum_{n>=2} Upsilon1[p, n]
                     if (cntp > 0) {
-                        acc += pos_sum(c.P - rw.la[p], c.Q - rw.ls[p], (R)1, rw.lv[p]);
+                        const R2<R> ln = rw.Ln[p];
+                        acc += pos_sum(c.P - ln.x, c.Q - ln.y, (R)1, e.y);
                         for (int k = 1; k < cntp; ++k) {
                             const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
                             acc += pos_sum(c.P - sg.a, c.Q - sg.s, (R)sg.u, (R)sg.v);
@@ -508,7 +528,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
                 }
                 n_cand += 1;
                 n_seg += (unsigned)cntp;
-                const R rest = acc + fma(c.Bv, sumM, Mxr * c.Av);
+                const R rest = acc + (R)fma(bd, rc.tvb, rc.tvc);   // + sum_{n>=2} T^v_n
                 const R T = c.d1 + rest;
                 if (T <= bT) { bT = T; bj = j; brest = rest; }   // '>=' of Alg. 1 line 21
             }
@@ -520,10 +540,11 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
             R rest = (R)0;
             int j = -1;
             Cand<R> c;
+            const double bd = (double)(nc - ci);
             if (ci < nc) {
                 j = jlo + ci;
-                const int p = j - 1, b = i - j + 1;
-                c = cand_terms(rw, rc, p, b);
+                const int p = j - 1;
+                c = cand_terms(rw, D, rc, p, bd);
                 const int chunk = (Mx + gsz - 1) / gsz;
                 const int m0 = 1 + sub * chunk, m1 = min(Mx, m0 + chunk - 1);
                 rest = dense_sum(rw, pl, p, c.P, c.Q, m0, m1, Mx);
@@ -532,7 +553,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
             if (ci < nc && sub == 0) {
                 n_cand += 1;
                 n_seg += (unsigned)rw.cnt[j - 1];
-                rest = rest + fma(c.Bv, sumM, Mxr * c.Av);
+                rest = rest + (R)fma(bd, rc.tvb, rc.tvc);
                 bT = c.d1 + rest;
                 bj = j;
                 brest = rest;
@@ -546,14 +567,14 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
         if (lane == owner) {
             // eq:rg, eq:tt1, eq:tt2 with j* (reading A4: S[i] always set)
             S[i - 1] = (short)jj;
-            const int p = jj - 1, b = i - jj + 1;
-            const Cand<R> c = cand_terms(rw, rc, p, b);
-            rw.y0[i] = c.d0;
-            rw.y1[i] = c.d1;
-            rw.a0[i] = c.P;
-            rw.s0[i] = c.Q;
-            rw.es[i] = brest;
-            ovf = env_update(rw, pl, p, i, c.P, c.Q, c.Av, c.Bv, Mx, top) ? 1 : 0;
+            const int p = jj - 1;
+            const double bd = (double)(i - jj + 1);
+            const Cand<R> c = cand_terms(rw, D, rc, p, bd);
+            rw.Y[i] = R2<R>{c.d0, c.d1};
+            rw.A[i] = R2<R>{c.P, c.Q};
+            rw.E[i].x = brest;
+            const R Av = (R)fma(bd, rc.av, D.c2vv), Bv = (R)(bd * D.bvc);
+            ovf = env_update(rw, pl, p, i, c.P, c.Q, Av, Bv, Mx, top) ? 1 : 0;
         }
         top = __shfl_sync(0xffffffffu, top, owner);
         ovf = __shfl_sync(0xffffffffu, ovf, owner);
@@ -568,7 +589,6 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
     if (lane == 0) wc.rows += rows_done;
     return T_last;
 }
-
 
 // ------------------------------------------------------------ the fused kernel
 #ifndef SDEDGE_MINB
