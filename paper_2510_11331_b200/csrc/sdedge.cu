@@ -93,32 +93,28 @@ template <> struct Pair<double> { using T = double2; };
 template <> struct Pair<float> { using T = float2; };
 template <typename R> using R2 = typename Pair<R>::T;
 
+// One DP row (AoS).  80 B for fp64 (40 B for fp32): with consecutive rows on
+// consecutive lanes the 16-byte loads of a warp hit distinct banks, and one
+// address computation serves all five loads.
 template <typename R>
-struct Rows {
-    R2<R>* Y;          // (Upsilon[p,1,0], Upsilon[p,1,1])
-    R2<R>* A;          // Upsilon[p,n,0] = A.x + A.y (n-1), n >= 2
-    R2<R>* E;          // (sum_{n=2}^{N} Upsilon[p,n,1], last m of the first envelope segment)
-    R2<R>* Ln;         // first envelope segment's line (intercept, slope in m = n-1)
-    int *off, *cnt;    // extra segments pool[off .. off+cnt-2]; cnt = #segments
+struct alignas(sizeof(R2<R>)) RowRec {
+    R2<R> Y;           // (Upsilon[p,1,0], Upsilon[p,1,1])
+    R2<R> A;           // Upsilon[p,n,0] = A.x + A.y (n-1), n >= 2
+    R2<R> E;           // (sum_{n=2}^{N} Upsilon[p,n,1], last m of the first envelope segment)
+    R2<R> Ln;          // first envelope segment's line (intercept, slope in m = n-1)
+    int cnt, off;      // #segments; extra segments in pool[off .. off+cnt-2]
 };
 
 template <typename R>
 __host__ __device__ inline size_t rows_bytes(int K)
 {
-    // rounded to 16 B so that every warp's pair arrays stay 16-byte aligned (LDS.128)
-    return ((size_t)(K + 1) * (8 * sizeof(R) + 2 * sizeof(int)) + 15) & ~(size_t)15;
+    return ((size_t)(K + 1) * sizeof(RowRec<R>) + 15) & ~(size_t)15;
 }
 
 template <typename R>
-__device__ inline Rows<R> carve_rows(unsigned char* base, int K)
+__device__ inline RowRec<R>* carve_rows(unsigned char* base, int K)
 {
-    Rows<R> r;
-    const size_t n = (size_t)K + 1;
-    R2<R>* f = reinterpret_cast<R2<R>*>(base);
-    r.Y = f; r.A = f + n; r.E = f + 2 * n; r.Ln = f + 3 * n;
-    int* q = reinterpret_cast<int*>(f + 4 * n);
-    r.off = q; r.cnt = q + n;
-    return r;
+    return reinterpret_cast<RowRec<R>*>(base);
 }
 
 template <typename R>
@@ -225,14 +221,14 @@ template <typename R>
 struct Seg { int u, v; R a, s; };
 
 template <typename R>
-__device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, int k, int c, int Mx)
+__device__ inline Seg<R> get_seg(const RowRec<R>* rw, const Pool<R>& pl, int p, int k, int c, int Mx)
 {
     Seg<R> sg;
     if (k == 0) {
-        const R2<R> ln = rw.Ln[p];
-        sg.u = 1; sg.v = (int)rw.E[p].y; sg.a = ln.x; sg.s = ln.y;
+        const R2<R> ln = rw[p].Ln;
+        sg.u = 1; sg.v = (int)rw[p].E.y; sg.a = ln.x; sg.s = ln.y;
     } else {
-        const long long q = rw.off[p] + k - 1;
+        const long long q = rw[p].off + k - 1;
         sg.u = pl.u[q]; sg.a = pl.a[q]; sg.s = pl.s[q];
         sg.v = (k + 1 < c) ? pl.u[q + 1] - 1 : Mx;
     }
@@ -243,11 +239,11 @@ __device__ inline Seg<R> get_seg(const Rows<R>& rw, const Pool<R>& pl, int p, in
 // written: the O(N) inner loop of Alg. 1 line 15).  Flat loop so that lanes
 // with different segment boundaries stay converged.
 template <typename R>
-__device__ inline R dense_sum(const Rows<R>& rw, const Pool<R>& pl, int p, R P, R Q, int m0, int m1, int Mx)
+__device__ inline R dense_sum(const RowRec<R>* rw, const Pool<R>& pl, int p, R P, R Q, int m0, int m1, int Mx)
 {
     R acc = (R)0;
     if (m0 > m1) return acc;
-    const int cntp = rw.cnt[p];
+    const int cntp = rw[p].cnt;
     int k = 0;
     Seg<R> sg = get_seg(rw, pl, p, 0, cntp, Mx);
     while (sg.v < m0) { ++k; sg = get_seg(rw, pl, p, k, cntp, Mx); }
@@ -303,10 +299,10 @@ template <typename R>
 struct Cand { R d0, d1, P, Q; };
 
 template <typename R>
-__device__ inline Cand<R> cand_terms(const Rows<R>& rw, const DPConst& D, const RowCoef& rc, int p, double bd)
+__device__ inline Cand<R> cand_terms(const RowRec<R>* rw, const DPConst& D, const RowCoef& rc, int p, double bd)
 {
     Cand<R> c;
-    const R2<R> y = rw.Y[p], a = rw.A[p];
+    const R2<R> y = rw[p].Y, a = rw[p].A;
     c.d0 = y.x + (R)fma(bd, rc.td1, D.c2dg);             // eq:tt1 at n = 1
     c.d1 = rmax(c.d0, y.y) + (R)fma(bd, rc.tv1, D.c2vv);  // eq:tt2 at n = 1 (reading A1)
     c.P = a.x + (R)fma(bd, rc.ad, D.c2dg);               // Upsilon0 line of the candidate, n >= 2
@@ -374,37 +370,37 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
 // The set where the new line beats the convex env_p is one interval [mlo, mhi].
 // Executed by the single lane that owns j*; returns true on pool overflow.
 template <typename R>
-__device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R P, R Q, R Av, R Bv,
+__device__ bool env_update(RowRec<R>* rw, const Pool<R>& pl, int p, int i, R P, R Q, R Av, R Bv,
                            int Mx, long long& top)
 {
-    const int cntp = rw.cnt[p];
+    const int cntp = rw[p].cnt;
     const long long base = top;
-    rw.off[i] = (int)base;
-    if (cntp == 0) { rw.cnt[i] = 0; return false; }            // N = 1: no n >= 2 steps
+    rw[i].off = (int)base;
+    if (cntp == 0) { rw[i].cnt = 0; return false; }            // N = 1: no n >= 2 steps
     if (cntp == 1) {                                           // fast path: one old line on [1, Mx]
-        const R2<R> ln = rw.Ln[p];
+        const R2<R> ln = rw[p].Ln;
         const R ea = ln.x, es = ln.y;
         const R dP = P - ea, dQ = Q - es;
         const R Du = dP + dQ, Dv = fma(dQ, (R)Mx, dP);
         if (!(Du > (R)0) && !(Dv > (R)0)) {                    // old line everywhere
-            rw.Ln[i] = R2<R>{ea + Av, es + Bv}; rw.E[i].y = (R)Mx; rw.cnt[i] = 1;
+            rw[i].Ln = R2<R>{ea + Av, es + Bv}; rw[i].E.y = (R)Mx; rw[i].cnt = 1;
             return false;
         }
         if (Du > (R)0 && Dv > (R)0) {                          // new line everywhere
-            rw.Ln[i] = R2<R>{P + Av, Q + Bv}; rw.E[i].y = (R)Mx; rw.cnt[i] = 1;
+            rw[i].Ln = R2<R>{P + Av, Q + Bv}; rw[i].E.y = (R)Mx; rw[i].cnt = 1;
             return false;
         }
         if (base >= pl.cap) return true;
         if (Dv > (R)0) {                                       // old on [1, f-1], new on [f, Mx]
             const int f = first_pos(dP, dQ, 1, Mx);
-            rw.Ln[i] = R2<R>{ea + Av, es + Bv}; rw.E[i].y = (R)(f - 1);
+            rw[i].Ln = R2<R>{ea + Av, es + Bv}; rw[i].E.y = (R)(f - 1);
             pl.u[base] = f; pl.a[base] = P + Av; pl.s[base] = Q + Bv;
         } else {                                               // new on [1, l], old on [l+1, Mx]
             const int l = last_pos(dP, dQ, 1, Mx);
-            rw.Ln[i] = R2<R>{P + Av, Q + Bv}; rw.E[i].y = (R)l;
+            rw[i].Ln = R2<R>{P + Av, Q + Bv}; rw[i].E.y = (R)l;
             pl.u[base] = l + 1; pl.a[base] = ea + Av; pl.s[base] = es + Bv;
         }
-        rw.cnt[i] = 2;
+        rw[i].cnt = 2;
         top = base + 1;
         return false;
     }
@@ -425,13 +421,13 @@ __device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R
         }
     int nseg = 0;
     bool ovf = false;
-    rw.E[i].y = (R)Mx;
+    rw[i].E.y = (R)Mx;
     auto emit = [&](int u, R a, R s) {
         a += Av;
         s += Bv;
-        if (nseg == 0) { rw.Ln[i] = R2<R>{a, s}; }
+        if (nseg == 0) { rw[i].Ln = R2<R>{a, s}; }
         else {
-            if (nseg == 1) rw.E[i].y = (R)(u - 1);
+            if (nseg == 1) rw[i].E.y = (R)(u - 1);
             const long long q = base + nseg - 1;
             if (q >= pl.cap) ovf = true;
             else { pl.u[q] = u; pl.a[q] = a; pl.s[q] = s; }
@@ -449,18 +445,69 @@ __device__ bool env_update(const Rows<R>& rw, const Pool<R>& pl, int p, int i, R
             emit(sg.u, sg.a, sg.s);
         }
     }
-    rw.cnt[i] = nseg;
+    rw[i].cnt = nseg;
     top = base + (nseg > 1 ? nseg - 1 : 0);
     return ovf;
+}
+
+// sum over the integer sub-range of [u, v] where dP + dQ m > 0, when the sign
+// changes inside [u, v] (Du = value at u, Dv = value at v).  Rare path.
+template <typename R>
+__device__ __noinline__ R crossing_sum(R dP, R dQ, int u, int v, R Du, R Dv)
+{
+    if (Dv > (R)0) {                         // increasing: positive on [f, v]
+        const int f = first_pos(dP, dQ, u, v);
+        return (R)(v - f + 1) * (fma(dQ, (R)f, dP) + Dv) * (R)0.5;
+    }
+    const int l = last_pos(dP, dQ, u, v);    // decreasing: positive on [u, l]
+    return (R)(l - u + 1) * (Du + fma(dQ, (R)l, dP)) * (R)0.5;
+}
+
+// Segments k >= 1 of a multi-segment envelope (rare path).
+template <typename R>
+__device__ __noinline__ R extra_segments(const RowRec<R>* rw, const Pool<R>& pl, int p, int cntp, R P, R Q, int Mx)
+{
+    R pos = (R)0;
+    for (int k = 1; k < cntp; ++k) {
+        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+        pos += pos_sum(P - sg.a, Q - sg.s, (R)sg.u, (R)sg.v);
+    }
+    return pos;
+}
+
+// T_{i,j} of one candidate by the envelope closed form (ALGO_ENVELOPE), for
+// N >= 2 (the envelope is non-empty).  Branch-light: the first segment's
+// positive part is a select, crossings and further segments are rare calls.
+template <typename R>
+__device__ inline R env_cand(const RowRec<R>* rw, const Pool<R>& pl, const DPConst& D, const RowCoef& rc, int p,
+                             double bd, int Mx, R& rest, int& nseg)
+{
+    const RowRec<R>* q = rw + p;
+    const R2<R> y = q->Y, a = q->A, e = q->E, ln = q->Ln;
+    const int cntp = q->cnt;
+    const R Td1 = (R)fma(bd, rc.td1, D.c2dg), Tv1 = (R)fma(bd, rc.tv1, D.c2vv);
+    const R P = a.x + (R)fma(bd, rc.ad, D.c2dg), Q = a.y + (R)(bd * D.bdc);
+    const R base = e.x + (R)fma(bd, rc.tvb, rc.tvc);     // sum_{n>=2} (Upsilon1[p,n] + T^v_n)
+    const R d1 = rmax(y.x + Td1, y.y) + Tv1;             // eq:t_ij1 at n = 1
+    // first segment [1, e.y] with line ln: sum of max(P + Q m - ln(m), 0)
+    const R dP = P - ln.x, dQ = Q - ln.y;
+    const R Du = dP + dQ, Dv = fma(dQ, e.y, dP);
+    const bool pu = Du > (R)0, pv = Dv > (R)0;
+    R pos = (pu && pv) ? (Du + Dv) * e.y * (R)0.5 : (R)0;
+    if (pu != pv) pos = crossing_sum(dP, dQ, 1, (int)e.y, Du, Dv);
+    if (cntp > 1) pos += extra_segments(rw, pl, p, cntp, P, Q, Mx);
+    nseg = cntp;
+    rest = base + pos;
+    return d1 + rest;
 }
 
 // ------------------------------------------------------------ the DP of one gamma
 // Returns T_inf (= Upsilon[K,0,0]) or +inf if some row has no feasible batch;
 // sets *overflow if the segment pool ran out.  S[i-1] = j* (1-based).
 template <typename R, int ALGO>
-__device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> pl, int gamma,
+__device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, int gamma,
                            double alpha, double c1d, double c2d, double c1v, double c2v,
-                           short* S, bool* overflow, WorkCount& wc)
+                           short* S, bool* overflow, WorkCount& wc, long long* top_s)
 {
     const int lane = threadIdx.x & 31;
     const int K = C.K;
@@ -480,21 +527,22 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
     D.c2vv = c2v + C.dl;
     D.Mx = Mx;
     D.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
-    long long top = 0;                                           // pool bump pointer
     unsigned n_cand = 0, n_seg = 0;
 
     if (lane == 0) {                                             // row 0 == 0 (reading A3)
-        rw.Y[0] = R2<R>{(R)0, (R)0};
-        rw.A[0] = R2<R>{(R)0, (R)0};
-        rw.E[0] = R2<R>{(R)0, (R)Mx};
-        rw.Ln[0] = R2<R>{(R)0, (R)0};
-        rw.off[0] = 0;
-        rw.cnt[0] = Mx >= 1 ? 1 : 0;
+        rw[0].Y = R2<R>{(R)0, (R)0};
+        rw[0].A = R2<R>{(R)0, (R)0};
+        rw[0].E = R2<R>{(R)0, (R)Mx};
+        rw[0].Ln = R2<R>{(R)0, (R)0};
+        rw[0].off = 0;
+        rw[0].cnt = Mx >= 1 ? 1 : 0;
+        *top_s = 0;                                              // pool bump pointer (owner lanes only)
     }
     __syncwarp();
 
     double T_last = 0.0;
     int rows_done = 0;
+    bool ovf_any = false;
     for (int i = 1; i <= K; ++i) {
         const int jlo = sm.jlo[i - 1];       // memory window (Alg. 1 lines 10-13)
         if (jlo > i) { T_last = dinf(); break; }
@@ -504,30 +552,31 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
         int bj = -1;
         R brest = (R)0;
         const int nc = i - jlo + 1;
-        if (ALGO == SDEDGE_ALGO_ENVELOPE || nc >= 17) {
-            // one lane per candidate, ascending j per lane (so '<=' keeps the largest j)
+        if (ALGO == SDEDGE_ALGO_ENVELOPE && Mx >= 1) {
+            // one lane per candidate, two candidates (j, j+32) in flight per lane;
+            // ascending j per lane, so '<=' keeps the largest j
+            double bd = (double)(i - jlo - lane + 1);
+            for (int j = jlo + lane; j <= i; j += 64, bd -= 64.0) {
+                const bool two = j + 32 <= i;
+                R r0, r1;
+                int c0, c1;
+                const R T0 = env_cand(rw, pl, D, rc, j - 1, bd, Mx, r0, c0);
+                R T1 = env_cand(rw, pl, D, rc, two ? j + 31 : j - 1, two ? bd - 32.0 : bd, Mx, r1, c1);
+                if (!two) { T1 = kinf<R>(); c1 = 0; }
+                n_cand += 1 + two;
+                n_seg += (unsigned)(c0 + c1);
+                if (T0 <= bT) { bT = T0; bj = j; brest = r0; }   // '>=' of Alg. 1 line 21
+                if (T1 <= bT) { bT = T1; bj = j + 32; brest = r1; }
+            }
+        } else if (ALGO == SDEDGE_ALGO_ENVELOPE || nc >= 17) {
+            // DENSE (or N = 1): one lane per candidate, ascending j per lane
             double bd = (double)(i - jlo - lane + 1);
             for (int j = jlo + lane; j <= i; j += 32, bd -= 32.0) {
                 const int p = j - 1;
                 const Cand<R> c = cand_terms(rw, D, rc, p, bd);
-                const int cntp = rw.cnt[p];
-                R acc;
-                if (ALGO == SDEDGE_ALGO_ENVELOPE) {
-                    const R2<R> e = rw.E[p];
-                    acc = e.x;                                   // sum_{n>=2} Upsilon1[p, n]
-                    if (cntp > 0) {
-                        const R2<R> ln = rw.Ln[p];
-                        acc += pos_sum(c.P - ln.x, c.Q - ln.y, (R)1, e.y);
-                        for (int k = 1; k < cntp; ++k) {
-                            const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
-                            acc += pos_sum(c.P - sg.a, c.Q - sg.s, (R)sg.u, (R)sg.v);
-                        }
-                    }
-                } else {
-                    acc = dense_sum(rw, pl, p, c.P, c.Q, 1, Mx, Mx);
-                }
+                const R acc = dense_sum(rw, pl, p, c.P, c.Q, 1, Mx, Mx);
                 n_cand += 1;
-                n_seg += (unsigned)cntp;
+                n_seg += (unsigned)rw[p].cnt;
                 const R rest = acc + (R)fma(bd, rc.tvb, rc.tvc);   // + sum_{n>=2} T^v_n
                 const R T = c.d1 + rest;
                 if (T <= bT) { bT = T; bj = j; brest = rest; }   // '>=' of Alg. 1 line 21
@@ -552,7 +601,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
             for (int o = gsz >> 1; o > 0; o >>= 1) rest += __shfl_xor_sync(0xffffffffu, rest, o);
             if (ci < nc && sub == 0) {
                 n_cand += 1;
-                n_seg += (unsigned)rw.cnt[j - 1];
+                n_seg += (unsigned)rw[j - 1].cnt;
                 rest = rest + (R)fma(bd, rc.tvb, rc.tvc);
                 bT = c.d1 + rest;
                 bj = j;
@@ -561,28 +610,44 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, Rows<R> rw, Pool<R> 
         }
         R tmin;
         const int jj = warp_argmin(bT, bj, &tmin);
+        // Every lane prepares row i as if its own best candidate won (SIMD, so this
+        // overlaps the REDUX latency instead of serialising behind it); the owner of
+        // j* then only stores.  eq:rg, eq:tt1, eq:tt2 (reading A4: S[i] always set).
+        const int pb = bj > 0 ? bj - 1 : 0;
+        const double bdb = (double)(i - pb);
+        const Cand<R> cb = cand_terms(rw, D, rc, pb, bdb);
+        const R Avb = (R)fma(bdb, rc.av, D.c2vv), Bvb = (R)(bdb * D.bvc);
+        const int cntb = rw[pb].cnt;
+        const R2<R> lnb = rw[pb].Ln;
+        const R dPb = cb.P - lnb.x, dQb = cb.Q - lnb.y;
+        const bool pub = dPb + dQb > (R)0, pvb = fma(dQb, (R)Mx, dPb) > (R)0;
         if (jj < 0) { T_last = dinf(); break; }                // no finite candidate
-        const int owner = __ffs(__ballot_sync(0xffffffffu, bj == jj)) - 1;
-        int ovf = 0;
-        if (lane == owner) {
-            // eq:rg, eq:tt1, eq:tt2 with j* (reading A4: S[i] always set)
+        if (bj == jj) {                                        // the owner (exactly one lane)
             S[i - 1] = (short)jj;
-            const int p = jj - 1;
-            const double bd = (double)(i - jj + 1);
-            const Cand<R> c = cand_terms(rw, D, rc, p, bd);
-            rw.Y[i] = R2<R>{c.d0, c.d1};
-            rw.A[i] = R2<R>{c.P, c.Q};
-            rw.E[i].x = brest;
-            const R Av = (R)fma(bd, rc.av, D.c2vv), Bv = (R)(bd * D.bvc);
-            ovf = env_update(rw, pl, p, i, c.P, c.Q, Av, Bv, Mx, top) ? 1 : 0;
+            RowRec<R>* o = rw + i;
+            o->Y = R2<R>{cb.d0, cb.d1};
+            o->A = R2<R>{cb.P, cb.Q};
+            if (cntb == 1 && pub == pvb) {
+                // one old line and the new line does not cross it inside [1, Mx]
+                o->Ln = pub ? R2<R>{cb.P + Avb, cb.Q + Bvb} : R2<R>{lnb.x + Avb, lnb.y + Bvb};
+                o->E = R2<R>{brest, (R)Mx};
+                o->cnt = 1;
+                o->off = 0;
+            } else {
+                long long top = *top_s;
+                o->E.x = brest;
+                if (env_update(rw, pl, pb, i, cb.P, cb.Q, Avb, Bvb, Mx, top)) {
+                    ovf_any = true;
+                    o->cnt = min(o->cnt, 1);                   // keep later reads in bounds
+                }
+                *top_s = top;
+            }
         }
-        top = __shfl_sync(0xffffffffu, top, owner);
-        ovf = __shfl_sync(0xffffffffu, ovf, owner);
         __syncwarp();
         ++rows_done;
-        if (ovf) { *overflow = true; T_last = dinf(); break; }
         T_last = (double)tmin;
     }
+    if (__any_sync(0xffffffffu, ovf_any)) { *overflow = true; T_last = dinf(); }
     wc.cand += n_cand;
     wc.seg += n_seg;
     wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
@@ -607,12 +672,13 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
 
     // RSMEM is a template parameter so that the compiler sees shared-window
     // (32-bit, LDS/STS) addresses for the row state instead of generic ones.
-    Rows<R> rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)warp * rows_bytes<R>(K)
+    RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)warp * rows_bytes<R>(K)
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     __shared__ bool s_ovf;
     __shared__ unsigned long long s_work[4];
+    __shared__ long long s_top[kWarps];
     if (tid < 4) s_work[tid] = 0;
     WorkCount wc;
 
@@ -692,7 +758,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 if (gi >= ng) break;
                 bool ovf = false;
                 const double t = dp_gamma<R, ALGO>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
-                                                   sm.S + (size_t)gi * K, &ovf, wc);
+                                                   sm.S + (size_t)gi * K, &ovf, wc, &s_top[warp]);
                 if (lane == 0) {
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
