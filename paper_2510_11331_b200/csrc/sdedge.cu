@@ -40,7 +40,10 @@ int fail(int code, const char* msg)
     return code;
 }
 
-constexpr int kWarps = 4;                // warps (DP workers) per CTA
+#ifndef SDEDGE_WARPS
+#define SDEDGE_WARPS 2
+#endif
+constexpr int kWarps = SDEDGE_WARPS;     // warps (DP workers) per CTA
 constexpr int kThreads = kWarps * 32;
 
 // ------------------------------------------------------------ call constants
@@ -657,7 +660,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
 
 // ------------------------------------------------------------ the fused kernel
 #ifndef SDEDGE_MINB
-#define SDEDGE_MINB 4     // min resident CTAs per SM requested from ptxas (128-register cap)
+#define SDEDGE_MINB 8     // min resident CTAs per SM requested from ptxas (128-register cap)
 #endif
 
 template <typename R, int ALGO, int RSMEM>
