@@ -285,8 +285,8 @@ def main():
         te = max_over_ranks(f0.elapsed_time(f1) * 1e-3, dist, dev)
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         d2h = sum(v.numel() * v.element_size() for v in hout.values() if v is not None)
-        e2e = {"value": n * ws * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": ksteps, "entry": "sdedge_solve_batch_host"}
+        e2e = {"value": n * ws * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h * ws, "steps": ksteps, "entry": "sdedge_solve_batch_host"}
 
     # ---- roofline of the dominant kernel (solve_kernel<.., BIG=0>; the second
     # launch is the worst-case-pool pass, empty unless an envelope overflowed)

@@ -43,7 +43,11 @@ int fail(int code, const char* msg)
 #ifndef SDEDGE_WARPS
 #define SDEDGE_WARPS 2
 #endif
-constexpr int kWarps = SDEDGE_WARPS;     // warps (DP workers) per CTA
+constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
+// G = DPs per warp: with ALGO_ENVELOPE and small K a warp runs G independent DPs
+// (different gamma) side by side in G lane groups of 32/G lanes, so every
+// per-row instruction (stage constants, argmin, update) serves G DPs; for
+// large K one DP per warp keeps more warps resident (chosen in launch_all).
 constexpr int kThreads = kWarps * 32;
 
 // ------------------------------------------------------------ call constants
@@ -157,22 +161,22 @@ __device__ inline double dinf() { return __longlong_as_double(0x7ff0000000000000
 // Warp argmin over (T, j): smallest T, then the LARGEST j (reading A6: the
 // ">=" of Alg. 1 line 21).  T >= 0 or +inf, so its IEEE bit pattern orders
 // like an unsigned integer: three REDUX instructions instead of a shuffle tree.
-__device__ inline int warp_argmin(double t, int j, double* tmin)
+__device__ inline int warp_argmin(double t, int j, double* tmin, unsigned mask)
 {
     const unsigned long long key = (unsigned long long)__double_as_longlong(t);
     const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-    const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
-    const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+    const unsigned mhi = __reduce_min_sync(mask, hi);
+    const unsigned mlo = __reduce_min_sync(mask, hi == mhi ? lo : 0xffffffffu);
     *tmin = __hiloint2double((int)mhi, (int)mlo);
-    return __reduce_max_sync(0xffffffffu, (hi == mhi && lo == mlo) ? j : -1);
+    return __reduce_max_sync(mask, (hi == mhi && lo == mlo) ? j : -1);
 }
 
-__device__ inline int warp_argmin(float t, int j, float* tmin)
+__device__ inline int warp_argmin(float t, int j, float* tmin, unsigned mask)
 {
     const unsigned key = __float_as_uint(t);
-    const unsigned m = __reduce_min_sync(0xffffffffu, key);
+    const unsigned m = __reduce_min_sync(mask, key);
     *tmin = __uint_as_float(m);
-    return __reduce_max_sync(0xffffffffu, key == m ? j : -1);
+    return __reduce_max_sync(mask, key == m ? j : -1);
 }
 
 // First / last integer m in [u, v] with dP + dQ m > 0, given that the sign
@@ -336,7 +340,7 @@ struct Smem {
     unsigned char* rows; // [kWarps] row states when rows_in_smem
 };
 
-template <typename R>
+template <typename R, int G>
 __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
 {
     size_t b = 0;
@@ -345,7 +349,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
-    if (rows_in_smem) b += kWarps * rows_bytes<R>(K);
+    if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K);
     return b;
 }
 
@@ -497,7 +501,7 @@ __device__ inline R env_cand(const RowRec<R>* rw, const Pool<R>& pl, const DPCon
     const R Du = dP + dQ, Dv = fma(dQ, e.y, dP);
     const bool pu = Du > (R)0, pv = Dv > (R)0;
     R pos = (pu && pv) ? (Du + Dv) * e.y * (R)0.5 : (R)0;
-    if (pu != pv) pos = crossing_sum(dP, dQ, 1, (int)e.y, Du, Dv);
+    if (pu != pv && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)e.y, Du, Dv);
     if (cntp > 1) pos += extra_segments(rw, pl, p, cntp, P, Q, Mx);
     nseg = cntp;
     rest = base + pos;
@@ -507,12 +511,15 @@ __device__ inline R env_cand(const RowRec<R>* rw, const Pool<R>& pl, const DPCon
 // ------------------------------------------------------------ the DP of one gamma
 // Returns T_inf (= Upsilon[K,0,0]) or +inf if some row has no feasible batch;
 // sets *overflow if the segment pool ran out.  S[i-1] = j* (1-based).
-template <typename R, int ALGO>
+template <typename R, int ALGO, int G>
 __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, int gamma,
                            double alpha, double c1d, double c2d, double c1v, double c2v,
-                           short* S, bool* overflow, WorkCount& wc, long long* top_s)
+                           short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
 {
+    constexpr int GL = 32 / G;
     const int lane = threadIdx.x & 31;
+    const int gl = lane % GL;                                    // lane within the DP's group
+    const unsigned gmask = G == 1 ? 0xffffffffu : (((1u << GL) - 1u) << (lane - gl));
     const int K = C.K;
     const double L = expected_tokens(alpha, gamma);
     const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
@@ -532,7 +539,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     D.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
     unsigned n_cand = 0, n_seg = 0;
 
-    if (lane == 0) {                                             // row 0 == 0 (reading A3)
+    if (gl == 0) {                                               // row 0 == 0 (reading A3)
         rw[0].Y = R2<R>{(R)0, (R)0};
         rw[0].A = R2<R>{(R)0, (R)0};
         rw[0].E = R2<R>{(R)0, (R)Mx};
@@ -555,24 +562,24 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         int bj = -1;
         R brest = (R)0;
         const int nc = i - jlo + 1;
-        if (ALGO == SDEDGE_ALGO_ENVELOPE && Mx >= 1) {
-            // one lane per candidate, two candidates (j, j+32) in flight per lane;
+        if (ALGO == SDEDGE_ALGO_ENVELOPE) {
+            // one lane per candidate, two candidates (j, j+GL) in flight per lane;
             // ascending j per lane, so '<=' keeps the largest j
-            double bd = (double)(i - jlo - lane + 1);
-            for (int j = jlo + lane; j <= i; j += 64, bd -= 64.0) {
-                const bool two = j + 32 <= i;
+            double bd = (double)(i - jlo - gl + 1);
+            for (int j = jlo + gl; j <= i; j += 2 * GL, bd -= 2.0 * GL) {
+                const bool two = j + GL <= i;
                 R r0, r1;
                 int c0, c1;
                 const R T0 = env_cand(rw, pl, D, rc, j - 1, bd, Mx, r0, c0);
-                R T1 = env_cand(rw, pl, D, rc, two ? j + 31 : j - 1, two ? bd - 32.0 : bd, Mx, r1, c1);
+                R T1 = env_cand(rw, pl, D, rc, two ? j + GL - 1 : j - 1, two ? bd - GL : bd, Mx, r1, c1);
                 if (!two) { T1 = kinf<R>(); c1 = 0; }
                 n_cand += 1 + two;
                 n_seg += (unsigned)(c0 + c1);
                 if (T0 <= bT) { bT = T0; bj = j; brest = r0; }   // '>=' of Alg. 1 line 21
-                if (T1 <= bT) { bT = T1; bj = j + 32; brest = r1; }
+                if (T1 <= bT) { bT = T1; bj = j + GL; brest = r1; }
             }
-        } else if (ALGO == SDEDGE_ALGO_ENVELOPE || nc >= 17) {
-            // DENSE (or N = 1): one lane per candidate, ascending j per lane
+        } else if (nc >= 17) {
+            // DENSE: one lane per candidate, ascending j per lane
             double bd = (double)(i - jlo - lane + 1);
             for (int j = jlo + lane; j <= i; j += 32, bd -= 32.0) {
                 const int p = j - 1;
@@ -612,7 +619,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
             }
         }
         R tmin;
-        const int jj = warp_argmin(bT, bj, &tmin);
+        const int jj = warp_argmin(bT, bj, &tmin, gmask);
         // Every lane prepares row i as if its own best candidate won (SIMD, so this
         // overlaps the REDUX latency instead of serialising behind it); the owner of
         // j* then only stores.  eq:rg, eq:tt1, eq:tt2 (reading A4: S[i] always set).
@@ -625,8 +632,8 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         const R dPb = cb.P - lnb.x, dQb = cb.Q - lnb.y;
         const bool pub = dPb + dQb > (R)0, pvb = fma(dQb, (R)Mx, dPb) > (R)0;
         if (jj < 0) { T_last = dinf(); break; }                // no finite candidate
-        if (bj == jj) {                                        // the owner (exactly one lane)
-            S[i - 1] = (short)jj;
+        if (bj == jj) {                                        // the owner (exactly one lane per group)
+            if (S) S[i - 1] = (short)jj;
             RowRec<R>* o = rw + i;
             o->Y = R2<R>{cb.d0, cb.d1};
             o->A = R2<R>{cb.P, cb.Q};
@@ -650,11 +657,13 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         ++rows_done;
         T_last = (double)tmin;
     }
-    if (__any_sync(0xffffffffu, ovf_any)) { *overflow = true; T_last = dinf(); }
-    wc.cand += n_cand;
-    wc.seg += n_seg;
-    wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
-    if (lane == 0) wc.rows += rows_done;
+    if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
+    if (active) {
+        wc.cand += n_cand;
+        wc.seg += n_seg;
+        wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
+        if (gl == 0) wc.rows += rows_done;
+    }
     return T_last;
 }
 
@@ -663,7 +672,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
 #define SDEDGE_MINB 8     // min resident CTAs per SM requested from ptxas (128-register cap)
 #endif
 
-template <typename R, int ALGO, int RSMEM>
+template <typename R, int ALGO, int RSMEM, int G>
 __global__ void __launch_bounds__(kThreads, SDEDGE_MINB)
 solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws, int BIG)
 {
@@ -671,17 +680,19 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     const int K = C.K, ng = C.ng;
     const Smem sm = carve_smem(smem_raw, K, ng);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long slot = (long long)blockIdx.x * kWarps + warp;
+    constexpr int GL = 32 / G;
+    const int grp = lane / GL;
+    const long long slot = ((long long)blockIdx.x * kWarps + warp) * G + grp;   // one DP per (warp, group)
 
     // RSMEM is a template parameter so that the compiler sees shared-window
     // (32-bit, LDS/STS) addresses for the row state instead of generic ones.
-    RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)warp * rows_bytes<R>(K)
+    RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)(warp * G + grp) * rows_bytes<R>(K)
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     __shared__ bool s_ovf;
     __shared__ unsigned long long s_work[4];
-    __shared__ long long s_top[kWarps];
+    __shared__ long long s_top[kWarps * G];
     if (tid < 4) s_work[tid] = 0;
     WorkCount wc;
 
@@ -755,14 +766,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         // ---- P3: each warp pulls gamma values and runs Algorithm 1
         if (!bad && !bad_alpha) {
             for (;;) {
-                int gi = 0;
-                if (lane == 0) gi = atomicAdd(&sm.ctl[0], 1);
-                gi = __shfl_sync(0xffffffffu, gi, 0);
-                if (gi >= ng) break;
+                int gi0 = 0;
+                if (lane == 0) gi0 = atomicAdd(&sm.ctl[0], G);
+                gi0 = __shfl_sync(0xffffffffu, gi0, 0);
+                if (gi0 >= ng) break;
+                int gi = gi0 + grp;
+                const bool active = gi < ng;       // an idle group repeats gi0 without writing
+                if (!active) gi = gi0;
                 bool ovf = false;
-                const double t = dp_gamma<R, ALGO>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
-                                                   sm.S + (size_t)gi * K, &ovf, wc, &s_top[warp]);
-                if (lane == 0) {
+                const double t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
+                                                   active ? sm.S + (size_t)gi * K : nullptr, &ovf, wc,
+                                                   &s_top[warp * G + grp], active);
+                if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
                 }
@@ -900,7 +915,7 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
         }                                                                       \
     } while (0)
 
-template <typename R, int ALGO>
+template <typename R, int ALGO, int G>
 int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long n, cudaStream_t st, int flags)
 {
     int dev = 0, nsm = 0, max_smem = 0;
@@ -911,12 +926,16 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     Consts C = C0;
     const size_t rb = rows_bytes<R>(C.K);
     // row state in shared memory when it keeps >= 3 CTAs (12 warps) per SM
-    C.rows_in_smem = smem_bytes<R>(C.K, C.ng, 1) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
-    const size_t sb = smem_bytes<R>(C.K, C.ng, C.rows_in_smem);
+#ifdef SDEDGE_ROWS_GLOBAL
+    C.rows_in_smem = 0;
+#else
+    C.rows_in_smem = smem_bytes<R, G>(C.K, C.ng, 1) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
+#endif
+    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem);
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
-    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1> : solve_kernel<R, ALGO, 0>;
+    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1, G> : solve_kernel<R, ALGO, 0, G>;
     auto k_big = k_main;
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
@@ -932,8 +951,8 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     const long long cap_main = (flags & SDEDGE_FLAG_TINY_POOL) ? 8LL : (4LL * (C.K + 1) + 64 + 7) & ~7LL;
     const long long cap_big = ((long long)C.K * (C.K + 1) + 64 + 7) & ~7LL;
     long long grid_big = std::max(1LL, std::min((long long)nsm,
-                                  (2LL << 30) / (long long)(kWarps * pool_bytes<R>(cap_big))));
-    const long long slots = grid * kWarps, slots_big = grid_big * kWarps;
+                                  (2LL << 30) / (long long)(kWarps * G * pool_bytes<R>(cap_big))));
+    const long long slots = grid * kWarps * G, slots_big = grid_big * kWarps * G;
 
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
@@ -988,11 +1007,19 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
                 reinterpret_cast<unsigned long long*>(o->work_counters)};
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
-    if (p->precision == 0)
-        return p->algo == SDEDGE_ALGO_DENSE ? launch_all<double, SDEDGE_ALGO_DENSE>(C, in, out, n, st, p->flags)
-                                            : launch_all<double, SDEDGE_ALGO_ENVELOPE>(C, in, out, n, st, p->flags);
-    return p->algo == SDEDGE_ALGO_DENSE ? launch_all<float, SDEDGE_ALGO_DENSE>(C, in, out, n, st, p->flags)
-                                        : launch_all<float, SDEDGE_ALGO_ENVELOPE>(C, in, out, n, st, p->flags);
+    // DPs per warp (envelope): 4 for small K, 2 for medium, 1 for large (r01 sweep)
+    const int G = p->algo == SDEDGE_ALGO_DENSE ? 1 : (p->K <= 48 ? 4 : p->K <= 96 ? 2 : 1);
+    const int f = p->flags;
+    if (p->precision == 0) {
+        if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<double, SDEDGE_ALGO_DENSE, 1>(C, in, out, n, st, f);
+        if (G == 4) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 4>(C, in, out, n, st, f);
+        if (G == 2) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 2>(C, in, out, n, st, f);
+        return launch_all<double, SDEDGE_ALGO_ENVELOPE, 1>(C, in, out, n, st, f);
+    }
+    if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<float, SDEDGE_ALGO_DENSE, 1>(C, in, out, n, st, f);
+    if (G == 4) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 4>(C, in, out, n, st, f);
+    if (G == 2) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 2>(C, in, out, n, st, f);
+    return launch_all<float, SDEDGE_ALGO_ENVELOPE, 1>(C, in, out, n, st, f);
 }
 
 }  // namespace
