@@ -243,24 +243,33 @@ __device__ inline Seg<R> get_seg(const RowRec<R>* rw, const Pool<R>& pl, int p, 
 }
 
 // sum_{m=m0}^{m1} max(P + Q m, env_p(m)), one step at a time (eq:t_ij1 as
-// written: the O(N) inner loop of Alg. 1 line 15).  Flat loop so that lanes
-// with different segment boundaries stay converged.
+// written: the O(N) inner loop of Alg. 1 line 15).  Per segment, four steps per
+// iteration with four accumulators (independent FP64 chains); the step value
+// m is one shared register, the other three lines are pre-shifted by Q and s.
 template <typename R>
 __device__ inline R dense_sum(const RowRec<R>* rw, const Pool<R>& pl, int p, R P, R Q, int m0, int m1, int Mx)
 {
-    R acc = (R)0;
-    if (m0 > m1) return acc;
+    R acc0 = (R)0, acc1 = (R)0, acc2 = (R)0, acc3 = (R)0;
+    if (m0 > m1) return acc0;
     const int cntp = rw[p].cnt;
-    int k = 0;
-    Seg<R> sg = get_seg(rw, pl, p, 0, cntp, Mx);
-    while (sg.v < m0) { ++k; sg = get_seg(rw, pl, p, k, cntp, Mx); }
-    R x = (R)m0;
-    for (int m = m0; m <= m1; ++m) {
-        if (m > sg.v) { ++k; sg = get_seg(rw, pl, p, k, cntp, Mx); }
-        acc += rmax(fma(Q, x, P), fma(sg.s, x, sg.a));
-        x += (R)1;
+    for (int k = 0; k < cntp; ++k) {
+        const Seg<R> sg = get_seg(rw, pl, p, k, cntp, Mx);
+        const int u = max(sg.u, m0), v = min(sg.v, m1);
+        if (sg.u > m1) break;
+        if (u > v) continue;
+        const R P1 = P + Q, P2 = P1 + Q, P3 = P2 + Q;
+        const R a1 = sg.a + sg.s, a2 = a1 + sg.s, a3 = a2 + sg.s;
+        R x = (R)u;
+        int m = u;
+        for (; m + 3 <= v; m += 4, x += (R)4) {
+            acc0 += rmax(fma(Q, x, P), fma(sg.s, x, sg.a));
+            acc1 += rmax(fma(Q, x, P1), fma(sg.s, x, a1));
+            acc2 += rmax(fma(Q, x, P2), fma(sg.s, x, a2));
+            acc3 += rmax(fma(Q, x, P3), fma(sg.s, x, a3));
+        }
+        for (; m <= v; ++m, x += (R)1) acc0 += rmax(fma(Q, x, P), fma(sg.s, x, sg.a));
     }
-    return acc;
+    return (acc0 + acc1) + (acc2 + acc3);
 }
 
 // Stage-time coefficients (D1: Appendix-A closed forms of eq:d_latency /
@@ -1046,6 +1055,10 @@ int sdedge_solve_batch(const sdedge_scenarios* s, int64_t n, const sdedge_params
 int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
                             sdedge_schedule* o)
 {
+    // Host buffers in, host buffers out.  The batch is cut into chunks that
+    // alternate between two internal streams, so the H2D copy of chunk c+1 and
+    // the D2H copy of chunk c-1 overlap the solve of chunk c; the caller's
+    // stream is joined at the end (one cudaMemcpyAsync per array and chunk).
     g_err[0] = 0;
     g_launches = 0;
     int rc = validate(s, n, p, out_latency, o);
@@ -1062,28 +1075,61 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
                  oW = take(bW), oSt = take(bS);
     unsigned char* d = nullptr;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&d), off, st));
-    CU(cudaMemcpyAsync(d + oI, s->input_len, bI, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d + oP, s->tx_power_w, bD, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d + oG, s->gain, bD, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(d + oA, s->alpha, bA, cudaMemcpyHostToDevice, st));
-    if (bC) CU(cudaMemcpyAsync(d + oC, s->coeffs, bC, cudaMemcpyHostToDevice, st));
-    sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI), reinterpret_cast<double*>(d + oP),
-                        reinterpret_cast<double*>(d + oG), reinterpret_cast<double*>(d + oA),
-                        bC ? reinterpret_cast<double*>(d + oC) : nullptr};
-    sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm), reinterpret_cast<int32_t*>(d + oM),
-                         reinterpret_cast<int32_t*>(d + oBe), reinterpret_cast<int32_t*>(d + oOr),
-                         bW ? reinterpret_cast<double*>(d + oW) : nullptr, reinterpret_cast<int32_t*>(d + oSt),
-                         nullptr};
-    rc = solve_device(&ds, n, p, reinterpret_cast<double*>(d + oLat), &dsch);
-    if (rc) return rc;
-    CU(cudaMemcpyAsync(out_latency, d + oLat, bLat, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(o->gamma, d + oGm, bS, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(o->num_batches, d + oM, bS, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(o->batch_end, d + oBe, bI, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(o->order, d + oOr, bI, cudaMemcpyDeviceToHost, st));
-    if (bW) CU(cudaMemcpyAsync(o->bw_share, d + oW, bW, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(o->status, d + oSt, bS, cudaMemcpyDeviceToHost, st));
+    cudaStream_t ss[2] = {nullptr, nullptr};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    for (int q = 0; q < 2; ++q) CU(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
+    for (int q = 0; q < 3; ++q) CU(cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming));
+    CU(cudaEventRecord(ev[0], st));
+    for (int q = 0; q < 2; ++q) CU(cudaStreamWaitEvent(ss[q], ev[0], 0));
+
+    const long long nch = std::max(1LL, std::min(8LL, (long long)(n / 65536)));
+    const long long chunk = (n + nch - 1) / nch;
+    int launches = 0;
+    auto h2d = [&](size_t doff, const void* src, size_t row, long long a, long long m, cudaStream_t q) {
+        return cudaMemcpyAsync(d + doff + row * a, static_cast<const unsigned char*>(src) + row * a, row * m,
+                               cudaMemcpyHostToDevice, q);
+    };
+    auto d2h = [&](void* dst, size_t doff, size_t row, long long a, long long m, cudaStream_t q) {
+        return cudaMemcpyAsync(static_cast<unsigned char*>(dst) + row * a, d + doff + row * a, row * m,
+                               cudaMemcpyDeviceToHost, q);
+    };
+    for (long long c = 0; c < nch; ++c) {
+        const long long a = c * chunk, m = std::min(chunk, (long long)n - a);
+        if (m <= 0) break;
+        cudaStream_t q = ss[c & 1];
+        CU(h2d(oI, s->input_len, K * 4, a, m, q));
+        CU(h2d(oP, s->tx_power_w, K * 8, a, m, q));
+        CU(h2d(oG, s->gain, K * 8, a, m, q));
+        CU(h2d(oA, s->alpha, 8, a, m, q));
+        if (bC) CU(h2d(oC, s->coeffs, 32, a, m, q));
+        sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI) + a * K, reinterpret_cast<double*>(d + oP) + a * K,
+                            reinterpret_cast<double*>(d + oG) + a * K, reinterpret_cast<double*>(d + oA) + a,
+                            bC ? reinterpret_cast<double*>(d + oC) + a * 4 : nullptr};
+        sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm) + a, reinterpret_cast<int32_t*>(d + oM) + a,
+                             reinterpret_cast<int32_t*>(d + oBe) + a * K, reinterpret_cast<int32_t*>(d + oOr) + a * K,
+                             bW ? reinterpret_cast<double*>(d + oW) + a * K : nullptr,
+                             reinterpret_cast<int32_t*>(d + oSt) + a, nullptr};
+        sdedge_params pc = *p;
+        pc.stream = q;
+        rc = solve_device(&ds, m, &pc, reinterpret_cast<double*>(d + oLat) + 3 * a, &dsch);
+        if (rc) return rc;
+        launches += g_launches;
+        CU(d2h(out_latency, oLat, 24, a, m, q));
+        CU(d2h(o->gamma, oGm, 4, a, m, q));
+        CU(d2h(o->num_batches, oM, 4, a, m, q));
+        CU(d2h(o->batch_end, oBe, K * 4, a, m, q));
+        CU(d2h(o->order, oOr, K * 4, a, m, q));
+        if (bW) CU(d2h(o->bw_share, oW, K * 8, a, m, q));
+        CU(d2h(o->status, oSt, 4, a, m, q));
+    }
+    for (int q = 0; q < 2; ++q) {
+        CU(cudaEventRecord(ev[1 + q], ss[q]));
+        CU(cudaStreamWaitEvent(st, ev[1 + q], 0));
+    }
     CU(cudaFreeAsync(d, st));
+    for (int q = 0; q < 2; ++q) CU(cudaStreamDestroy(ss[q]));   // released once their work drains
+    for (int q = 0; q < 3; ++q) CU(cudaEventDestroy(ev[q]));
+    g_launches = launches;
     return 0;
 }
 

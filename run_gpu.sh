@@ -1,2 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -2 gpurun_out/pytest_gpu.log
-for c in C4 C3; do timeout 300 python bench.py --config $c --n 200000 --steps 3 --warmup 2 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value']), d['roofline']['frac'])"; done
+timeout 600 python bench.py --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C4', round(d['value']), d['roofline']['frac'], 'e2e', round(d['e2e']['value']))"
+timeout 600 python bench.py --algo dense --n 50000 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dense', round(d['value']), d['roofline']['frac'])"

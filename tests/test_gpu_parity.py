@@ -242,3 +242,17 @@ def test_pipe_peak_runs():
     import paper_2510_11331_b200 as sd
     ops, t = sd.sdedge_pipe_peak(False)
     assert ops > 1e12 and t > 0
+
+
+def test_host_entry_point_chunked():
+    """More than one 65536-scenario chunk through the pipelined host entry:
+    identical bytes to the device entry point."""
+    import paper_2510_11331_b200 as sd
+    pd = scengen.params("68M-7B", K=32, gamma_min=1, gamma_max=8)
+    sc = scengen.generate(3, 32, 0, 200_000)
+    d = gpu_solve(pd, sc)
+    h = sd.solve_host(pd, *(torch.from_numpy(sc[k]).pin_memory() for k in ("I", "p", "g", "alpha")))
+    torch.cuda.synchronize()
+    h = to_numpy(h)
+    for k in d:
+        assert np.array_equal(d[k], h[k]), k
