@@ -208,9 +208,20 @@ def main():
     import paper_2510_11331_b200 as sd
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    if ws > 1:
+        # NCCL may print its version banner on stdout when the communicator is
+        # created; keep stdout for the single JSON line.
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     dev = torch.device("cuda", local)
     sd.lib()
 

@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define SDEDGE_ABI_VERSION 1
+#define SDEDGE_ABI_VERSION 2
 #define SDEDGE_MAX_K 1024
 
 typedef struct {
@@ -67,6 +67,24 @@ typedef enum {
 } sdedge_algo;
 
 #define SDEDGE_FLAG_TINY_POOL 1
+
+/* Bandwidth policies (P:580-616 and the uniform baseline of P:936-940). */
+typedef enum {
+    SDEDGE_BW_OPTIMAL = 0,       /* closed-form w*_k of eq:opt_w (the proposed policy)           */
+    SDEDGE_BW_UNIFORM = 1        /* w_k = 1/K, T_com = max_k T_k,com (eq:ul_latency)              */
+} sdedge_bw_policy;
+
+/* Batching policies: the proposed Algorithm 1 and the paper's baselines
+ * (Sec. IV); gamma is always enumerated over
+ * [gamma_min, gamma_max] (fixed speculation length "FSL" = gamma_min = gamma_max = 7). */
+typedef enum {
+    SDEDGE_BATCH_PROPOSED = 0,   /* Algorithm 1 with the pipelined cost              */
+    SDEDGE_BATCH_NO_PIPELINE = 1,/* "SD w/o pipeline": Algorithm 1 with T_n = sum_m (T^d + T^v)  */
+    SDEDGE_BATCH_NONE = 2,       /* "No batching": one task per batch, pipelined        */
+    SDEDGE_BATCH_STATIC = 3,     /* fixed batch size `static_batch` in sorted order  */
+    SDEDGE_BATCH_MAX = 4,        /* largest memory-feasible size for the longest input */
+    SDEDGE_BATCH_HEURISTIC = 5   /* sizes 2,3,... until the latency stops improving */
+} sdedge_batch_policy;
 
 typedef struct {
     sdedge_model draft, verify;  /* SBS draft / MBS verify models                    */
@@ -86,6 +104,10 @@ typedef struct {
                                     envelope pool, forcing the worst-case second pass)       */
     double  downlink_s;          /* >= 0, added to every verify stage (P:424-427 says 0)     */
     void*   stream;              /* cudaStream_t                                              */
+    int32_t bandwidth_policy;    /* sdedge_bw_policy (0 = the paper's policy)                 */
+    int32_t batching_policy;     /* sdedge_batch_policy (0 = the paper's policy)              */
+    int32_t static_batch;        /* batch size of SDEDGE_BATCH_STATIC, >= 1                   */
+    int32_t reserved;            /* must be 0                                                 */
 } sdedge_params;
 
 typedef struct {

@@ -33,7 +33,8 @@ class Params(C.Structure):
                 ("c1d", C.c_double), ("c2d", C.c_double), ("c1v", C.c_double), ("c2v", C.c_double),
                 ("Bw", C.c_double), ("sigma2", C.c_double), ("lambda_", C.c_double),
                 ("gamma_s", C.c_int64), ("K", C.c_int32), ("O_max", C.c_int32),
-                ("gamma_min", C.c_int32), ("gamma_max", C.c_int32), ("downlink_s", C.c_double)]
+                ("gamma_min", C.c_int32), ("gamma_max", C.c_int32), ("downlink_s", C.c_double),
+                ("bw_policy", C.c_int32), ("batch_policy", C.c_int32), ("static_batch", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -78,6 +79,12 @@ def lib():
         L.orc_dp.restype = C.c_double
         L.orc_dp.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_f64,
                              P_i64, C.c_int, C.c_int]
+        L.orc_eval_plan_nopipe.restype = C.c_double
+        L.orc_eval_plan_nopipe.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, C.c_int, P_i32]
+        L.orc_dp_nopipe.restype = C.c_double
+        L.orc_dp_nopipe.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_f64, P_i64]
+        L.orc_fixed_plan.restype = C.c_int
+        L.orc_fixed_plan.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32]
         L.orc_solve.restype = None
         L.orc_solve.argtypes = [C.POINTER(Params), P_i32, P_f64, P_f64, C.c_double, P_f64,
                                 C.POINTER(Result), P_i32, P_i32, P_f64, P_f64]
@@ -98,7 +105,8 @@ def make_params(d: dict) -> Params:
     return Params(Jd, h1d, h2d, Jv, h1v, h2v, d["c1_draft"], d["c2_draft"], d["c1_verify"],
                   d["c2_verify"], d["bandwidth_hz"], d["noise_w"], d.get("lambda_bits", 0.0),
                   int(d["mem_capacity_bytes"]), d["K"], d["O_max"], d["gamma_min"], d["gamma_max"],
-                  d.get("downlink_s", 0.0))
+                  d.get("downlink_s", 0.0), d.get("bandwidth_policy", 0), d.get("batching_policy", 0),
+                  d.get("static_batch", 4))
 
 
 def _p(a, t):
@@ -184,6 +192,36 @@ def dp(pd, Is, alpha, gamma, coeffs=None, force_row=0, force_j=0):
     t = lib().orc_dp(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma,
                      _p(S, C.c_int32), _p(gap, C.c_double), C.byref(W), force_row, force_j)
     return t, S, gap, W.value
+
+
+def eval_plan_nopipe(pd, Is, alpha, gamma, batch_end, coeffs=None):
+    P = make_params(dict(pd, K=len(Is)))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    be = np.ascontiguousarray(batch_end, dtype=np.int32)
+    co = _co(coeffs)
+    return lib().orc_eval_plan_nopipe(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma,
+                                      len(be), _p(be, C.c_int32))
+
+
+def dp_nopipe(pd, Is, alpha, gamma, coeffs=None):
+    P = make_params(dict(pd, K=len(Is)))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    S = np.zeros(len(Is), np.int32)
+    gap = np.full(len(Is), np.inf)
+    W = C.c_int64(0)
+    co = _co(coeffs)
+    t = lib().orc_dp_nopipe(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma,
+                            _p(S, C.c_int32), _p(gap, C.c_double), C.byref(W))
+    return t, S, gap, W.value
+
+
+def fixed_plan(pd, Is, alpha, gamma, coeffs=None):
+    P = make_params(dict(pd, K=len(Is)))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    ends = np.zeros(len(Is) + 1, np.int32)
+    co = _co(coeffs)
+    M = lib().orc_fixed_plan(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma, _p(ends, C.c_int32))
+    return [int(x) for x in ends[:M]]
 
 
 def backtrack(S):

@@ -116,6 +116,19 @@ double orc_bandwidth(const orc_params* P, const int32_t* I, const double* p, con
 {
     const int K = P->K;
     const double lam = P->lambda > 0 ? P->lambda : 16.0 * (P->h1d + P->h1v); /* P:439 */
+    if (P->bw_policy == 1) {
+        /* uniform scheme (P:938-940): w_k = 1/K; T_com = max_k T_k,com (eq:ul_latency_k, eq:ul_latency) */
+        double tmax = 0.0;
+        for (int k = 0; k < K; ++k) {
+            double wk = 1.0 / K;
+            double snr = p[k] * g[k] / P->sigma2;
+            double r = wk * P->Bw * log2(1.0 + snr);
+            double t = lam * I[k] / r;
+            if (t > tmax) tmax = t;
+            if (w) w[k] = wk;
+        }
+        return tmax;
+    }
     double tcom = 0.0, denom = 0.0;
     for (int k = 0; k < K; ++k) {
         double snr = p[k] * g[k] / P->sigma2;
@@ -157,6 +170,119 @@ double orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, d
         Tinf += C; /* T_n = C_{n,M} */
     }
     return Tinf;
+}
+
+double orc_eval_plan_nopipe(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                            int gamma, int M, const int32_t* batch_end)
+{
+    double L = orc_expected_tokens(alpha, gamma);
+    int N = orc_decode_steps(P->O_max, L);
+    for (int m = 0; m < M; ++m) {
+        int start = m ? batch_end[m - 1] + 1 : 1;
+        if (!batch_fits(P, batch_end[m] - start + 1, Is[batch_end[m] - 1])) return INFINITY;
+    }
+    double Tinf = 0.0;
+    for (int n = 1; n <= N; ++n) {
+        double Tn = 0.0;
+        for (int m = 0; m < M; ++m) {
+            int start = m ? batch_end[m - 1] + 1 : 1;
+            int b = batch_end[m] - start + 1;
+            int32_t Im = Is[batch_end[m] - 1];
+            Tn += orc_draft_time(P, co, b, Im, gamma, L, n) + orc_verify_time(P, co, b, Im, gamma, L, n);
+        }
+        Tinf += Tn;
+    }
+    return Tinf;
+}
+
+double orc_dp_nopipe(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                     int32_t* S, double* row_gap, int64_t* W)
+{
+    /* Algorithm 1's loop structure with the sequential (no-overlap) step cost:
+     * T_{i,j} = Upsilon[j-1,0,0] + sum_n (T^d_n + T^v_n) -- additive, so exact. */
+    const int K = P->K;
+    double L = orc_expected_tokens(alpha, gamma);
+    int N = orc_decode_steps(P->O_max, L);
+    double* V = (double*)calloc((size_t)K + 1, sizeof(double));
+    double result = 0.0;
+    for (int i = 1; i <= K; ++i) {
+        double best = INFINITY, second = INFINITY;
+        int jstar = 0;
+        int32_t Im = Is[i - 1];
+        for (int j = 1; j <= i; ++j) {
+            int b = i - j + 1;
+            if (!batch_fits(P, b, Im)) continue;
+            double temp = V[j - 1];
+            for (int n = 1; n <= N; ++n)
+                temp += orc_draft_time(P, co, b, Im, gamma, L, n) + orc_verify_time(P, co, b, Im, gamma, L, n);
+            if (W) *W += N;
+            if (best >= temp) { second = best; best = temp; jstar = j; }
+            else if (temp < second) second = temp;
+        }
+        if (jstar == 0) { result = INFINITY; if (S) S[i - 1] = 0; break; }
+        V[i] = best;
+        if (S) S[i - 1] = jstar;
+        if (row_gap)
+            row_gap[i - 1] = isinf(second) ? INFINITY : second == best ? 0.0 : (second - best) / fabs(best);
+        result = best;
+    }
+    free(V);
+    return result;
+}
+
+static int equal_plan(int K, int b, int32_t* ends)
+{
+    int M = 0;
+    for (int e = b; e < K; e += b) ends[M++] = e;
+    ends[M++] = K;
+    return M;
+}
+
+int orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                   int32_t* ends)
+{
+    const int K = P->K;
+    int M = 0;
+    switch (P->batch_policy) {
+    case 2: /* no batching: one task at a time */
+        for (int k = 1; k <= K; ++k) ends[M++] = k;
+        break;
+    case 3: /* static batching: fixed small batch size, contiguous in sorted order */
+        M = equal_plan(K, P->static_batch < K ? P->static_batch : K, ends);
+        break;
+    case 4: { /* max batching: largest b for which a batch of b of the arriving
+                 tasks' longest input (and O_max) fits the SBS memory (reading B4) */
+        int b = 0;
+        while (b < K && batch_fits(P, b + 1, Is[K - 1])) ++b;
+        if (b < 1) return 0;
+        M = equal_plan(K, b, ends);
+        break;
+    }
+    case 5: { /* heuristic (reading B5): batch size 2, 3, ... until the
+                 pipelined latency stops improving (or memory binds) */
+        int32_t tmp[1024 + 1];
+        int bbest = 1;
+        double tbest = INFINITY;
+        for (int b = (K >= 2 ? 2 : 1); b <= K; ++b) {
+            int Mt = equal_plan(K, b, tmp);
+            double t = orc_eval_plan(P, co, Is, alpha, gamma, Mt, tmp);
+            if (!(t < tbest) && !isinf(tbest)) break;   /* latency starts to degrade */
+            if (isinf(t)) break;                          /* memory binds */
+            tbest = t;
+            bbest = b;
+        }
+        if (isinf(tbest)) bbest = 1;                      /* even b = 2 infeasible: one at a time */
+        M = equal_plan(K, bbest, ends);
+        break;
+    }
+    default:
+        return 0;
+    }
+    for (int m = 0; m < M; ++m) {
+        int start = m ? ends[m - 1] + 1 : 1;
+        if (!batch_fits(P, ends[m] - start + 1, Is[ends[m] - 1])) return 0;
+    }
+    return M;
 }
 
 /* Algorithm 1 with readings A1 (bracket of eq:t_ij1), A3 (K+1
@@ -265,14 +391,31 @@ void orc_solve(const orc_params* P, const int32_t* I, const double* p, const dou
     for (int k = 0; k < K; ++k) Is[k] = I[order[k]];
 
     double best = INFINITY, second = INFINITY;
-    int gbest = -1;
+    int gbest = -1, Mbest = 0;
+    int32_t* ends = (int32_t*)malloc(sizeof(int32_t) * (K + 1));
+    int32_t* ends_best = (int32_t*)malloc(sizeof(int32_t) * (K + 1));
     for (int gm = P->gamma_min; gm <= P->gamma_max; ++gm) { /* P3 */
-        double t = orc_dp(P, coeffs4, Is, alpha, gm, S, gap, &R->W, 0, 0);
+        double t;
+        int Mg = 0;
+        if (P->batch_policy <= 1) {
+            for (int r = 0; r < K; ++r) gap[r] = INFINITY;
+            t = P->batch_policy == 0 ? orc_dp(P, coeffs4, Is, alpha, gm, S, gap, &R->W, 0, 0)
+                                     : orc_dp_nopipe(P, coeffs4, Is, alpha, gm, S, gap, &R->W);
+            if (!isinf(t)) {   /* backtracking (reading A5: i <- S[i] - 1) */
+                int tmp[1024 + 1], i = K;
+                while (i > 0) { tmp[Mg++] = i; i = S[i - 1] - 1; }
+                for (int m = 0; m < Mg; ++m) ends[m] = tmp[Mg - 1 - m];
+            }
+        } else {
+            Mg = orc_fixed_plan(P, coeffs4, Is, alpha, gm, ends);
+            t = Mg > 0 ? orc_eval_plan(P, coeffs4, Is, alpha, gm, Mg, ends) : INFINITY;
+            for (int r = 0; r < K; ++r) gap[r] = INFINITY;
+        }
         tinf_gamma[gm - P->gamma_min] = t;
         if (isinf(t)) continue;
         for (int r = 0; r < K; ++r)
             if (gap[r] < R->min_row_gap) { R->min_row_gap = gap[r]; R->gap_gamma = gm; R->gap_row = r + 1; }
-        if (t < best) { second = best; best = t; gbest = gm; memcpy(Sbest, S, sizeof(int32_t) * K); }
+        if (t < best) { second = best; best = t; gbest = gm; Mbest = Mg; memcpy(ends_best, ends, sizeof(int32_t) * Mg); }
         else if (t < second) second = t; /* smallest gamma wins ties (reading A7) */
     }
     if (gbest < 0) {
@@ -283,13 +426,10 @@ void orc_solve(const orc_params* P, const int32_t* I, const double* p, const dou
         R->T_inf = best;
         R->T = R->T_com + R->T_inf;
         R->gamma_gap = isinf(second) ? INFINITY : (second - best) / best;
-        /* backtracking (reading A5: i <- S[i] - 1) */
-        int tmp[1024 + 1];
-        int M = 0, i = K;
-        while (i > 0) { tmp[M++] = i; i = Sbest[i - 1] - 1; }
-        for (int m = 0; m < M; ++m) batch_end[m] = tmp[M - 1 - m];
-        R->M = M;
+        for (int m = 0; m < Mbest; ++m) batch_end[m] = ends_best[m];
+        R->M = Mbest;
     }
+    free(ends); free(ends_best);
     free(Is); free(S); free(Sbest); free(gap);
 }
 

@@ -32,6 +32,11 @@ typedef struct {
     int64_t gamma_s;             /* SBS memory capacity Gamma_s, bytes           */
     int32_t K, O_max, gamma_min, gamma_max;
     double  downlink_s;          /* optional per-step, per-batch verify add-on   */
+    int32_t bw_policy;           /* 0 optimal eq:opt_w, 1 uniform w_k = 1/K */
+    int32_t batch_policy;        /* 0 Algorithm 1 (pipelined), 1 SD w/o pipeline,
+                                    2 no batching, 3 static,
+                                    4 max batching, 5 heuristic */
+    int32_t static_batch;        /* batch size of policy 3                          */
 } orc_params;
 
 typedef struct {
@@ -72,6 +77,20 @@ double  orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, 
  * one row -- used by the near-tie branching replay. */
 double  orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
                int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j);
+
+/* "SD w/o pipeline" evaluation of a plan: every decoding step runs draft then
+ * verify of each batch sequentially, T_n = sum_m (T^d_{n,m} + T^v_{n,m}). */
+double  orc_eval_plan_nopipe(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                             int gamma, int M, const int32_t* batch_end);
+
+/* Algorithm 1 with the SD-w/o-pipeline cost (additive, exact). Same outputs as orc_dp. */
+double  orc_dp_nopipe(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                      int32_t* S, double* row_gap, int64_t* W);
+
+/* Fixed-plan batching policies 2..5 for one gamma: writes the plan (ends), returns M
+ * (0 if no memory-feasible plan exists). */
+int     orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                       int32_t* ends);
 
 /* Full solve of problem P for one scenario.
  * order[K], batch_end[K], w[K], tinf_gamma[gamma_max-gamma_min+1] are caller-owned. */

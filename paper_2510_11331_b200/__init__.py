@@ -17,6 +17,8 @@ __all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_pipe_peak", 
            "ALGO_ENVELOPE", "ALGO_DENSE", "EXPORTED_SYMBOLS", "lib"]
 
 ALGO_ENVELOPE, ALGO_DENSE = 0, 1
+BW_OPTIMAL, BW_UNIFORM = 0, 1
+BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC = range(6)
 FLAG_TINY_POOL = 1
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_last_launch_count",
                     "sdedge_last_error", "sdedge_abi_version", "sdedge_pipe_peak")
@@ -34,7 +36,8 @@ class SdedgeParams(C.Structure):
                 ("mem_capacity_bytes", C.c_int64), ("K", C.c_int32), ("O_max", C.c_int32),
                 ("gamma_min", C.c_int32), ("gamma_max", C.c_int32), ("precision", C.c_int32),
                 ("algo", C.c_int32), ("flags", C.c_int32), ("downlink_s", C.c_double),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("bandwidth_policy", C.c_int32), ("batching_policy", C.c_int32),
+                ("static_batch", C.c_int32), ("reserved", C.c_int32)]
 
 
 class SdedgeScenarios(C.Structure):
@@ -96,7 +99,8 @@ def make_params(d: dict, stream=None, precision: int | None = None, algo: int | 
                         int(d["mem_capacity_bytes"]), d["K"], d["O_max"], d["gamma_min"], d["gamma_max"],
                         d.get("precision", 0) if precision is None else precision,
                         d.get("algo", ALGO_ENVELOPE) if algo is None else algo, d.get("flags", 0),
-                        d.get("downlink_s", 0.0), st)
+                        d.get("downlink_s", 0.0), st, d.get("bandwidth_policy", 0),
+                        d.get("batching_policy", 0), d.get("static_batch", 4), 0)
 
 
 def _ptr(t):

@@ -57,6 +57,7 @@ struct Consts {
     double c1d, c2d, c1v, c2v;           // defaults when coeffs == NULL
     double Bw, sigma2, lambda, dl;
     long long gamma_s, Gp, kvunit;       // Gamma_s, Gamma_p (eq:memory_model), 4 Jd hd
+    int bw_policy, batch_policy, static_batch;   // SDEDGE_BW_* / SDEDGE_BATCH_* (paper baselines)
     int rows_in_smem;                    // DP row state in shared (1) or global (0) memory
     long long pool_cap;                  // envelope segments per warp slot
     long long rows_stride;               // bytes of one warp's global row state
@@ -341,6 +342,8 @@ struct Smem {
     int* Is;       // [K] sorted lengths
     int* ord;      // [K] sorted pos -> task
     short* jlo;    // [K] first feasible j of row i (memory window), > i if none
+    short* jf;     // [K] fixed-plan policies: start j of the batch ending at row i, 0 if none
+    short* jw;     // [kWarps][K] heuristic batching: the plan under evaluation
     short* S;      // [ng][K] boundaries (1-based j*)
     double* tinf;  // [ng]
     double* red;   // [2 * kWarps]
@@ -354,7 +357,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
-    b += (size_t)(ng + 1) * K * sizeof(short);
+    b += (size_t)(ng + 2 + kWarps) * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
@@ -370,6 +373,8 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     s.Is = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.ord = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
+    s.jf = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
+    s.jw = reinterpret_cast<short*>(base + b); b += (size_t)kWarps * K * sizeof(short);
     s.S = reinterpret_cast<short*>(base + b); b += (size_t)ng * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
@@ -523,7 +528,8 @@ __device__ inline R env_cand(const RowRec<R>* rw, const Pool<R>& pl, const DPCon
 template <typename R, int ALGO, int G>
 __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, int gamma,
                            double alpha, double c1d, double c2d, double c1v, double c2v,
-                           short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
+                           short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
+                           const short* jf)
 {
     constexpr int GL = 32 / G;
     const int lane = threadIdx.x & 31;
@@ -562,21 +568,54 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     double T_last = 0.0;
     int rows_done = 0;
     bool ovf_any = false;
+    const bool nopipe = C.batch_policy == SDEDGE_BATCH_NO_PIPELINE;
     for (int i = 1; i <= K; ++i) {
-        const int jlo = sm.jlo[i - 1];       // memory window (Alg. 1 lines 10-13)
-        if (jlo > i) { T_last = dinf(); break; }
+        int jlo = sm.jlo[i - 1];             // memory window (Alg. 1 lines 10-13)
+        int jhi = i;
+        if (jf) {                            // fixed plan: only the batch ending at i (if any)
+            const int jfi = jf[i - 1];
+            if (jfi == 0) continue;
+            if (jfi < jlo) { T_last = dinf(); break; }
+            jlo = jhi = jfi;
+        }
+        if (jlo > jhi) { T_last = dinf(); break; }
         const RowCoef rc = row_coef(D, sm.Is[i - 1]);
+        if (nopipe) {
+            // "SD w/o pipeline": T_n = sum_m (T^d + T^v), so T_{i,j} =
+            // Upsilon[j-1,0,0] + sum_n (T^d_n + T^v_n)(b, I_i), closed form in b.
+            const double slope = rc.td1 + rc.tv1 + D.Mx * (rc.ad + rc.av) + D.sumM * (D.bdc + D.bvc);
+            const double fixed = (D.c2dg + D.c2vv) * (D.Mx + 1.0);
+            R bT = kinf<R>();
+            int bj = -1;
+            double bd = (double)(i - jlo - gl + 1);
+            for (int j = jlo + gl; j <= jhi; j += GL, bd -= GL) {
+                const R T = rw[j - 1].E.x + (R)fma(bd, slope, fixed);
+                n_cand += 1;
+                if (T <= bT) { bT = T; bj = j; }
+            }
+            R tmin;
+            const int jj = warp_argmin(bT, bj, &tmin, gmask);
+            if (jj < 0) { T_last = dinf(); break; }
+            if (bj == jj) {
+                if (S) S[i - 1] = (short)jj;
+                rw[i].E = R2<R>{tmin, (R)0};
+            }
+            __syncwarp(gmask);
+            ++rows_done;
+            T_last = (double)tmin;
+            continue;
+        }
 
         R bT = kinf<R>();
         int bj = -1;
         R brest = (R)0;
-        const int nc = i - jlo + 1;
+        const int nc = jhi - jlo + 1;
         if (ALGO == SDEDGE_ALGO_ENVELOPE) {
             // one lane per candidate, two candidates (j, j+GL) in flight per lane;
             // ascending j per lane, so '<=' keeps the largest j
             double bd = (double)(i - jlo - gl + 1);
-            for (int j = jlo + gl; j <= i; j += 2 * GL, bd -= 2.0 * GL) {
-                const bool two = j + GL <= i;
+            for (int j = jlo + gl; j <= jhi; j += 2 * GL, bd -= 2.0 * GL) {
+                const bool two = j + GL <= jhi;
                 R r0, r1;
                 int c0, c1;
                 const R T0 = env_cand(rw, pl, D, rc, j - 1, bd, Mx, r0, c0);
@@ -590,7 +629,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         } else if (nc >= 17) {
             // DENSE: one lane per candidate, ascending j per lane
             double bd = (double)(i - jlo - lane + 1);
-            for (int j = jlo + lane; j <= i; j += 32, bd -= 32.0) {
+            for (int j = jlo + lane; j <= jhi; j += 32, bd -= 32.0) {
                 const int p = j - 1;
                 const Cand<R> c = cand_terms(rw, D, rc, p, bd);
                 const R acc = dense_sum(rw, pl, p, c.P, c.Q, 1, Mx, Mx);
@@ -608,7 +647,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
             R rest = (R)0;
             int j = -1;
             Cand<R> c;
-            const double bd = (double)(nc - ci);
+            const double bd = (double)(i - jlo - ci + 1);
             if (ci < nc) {
                 j = jlo + ci;
                 const int p = j - 1;
@@ -662,7 +701,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
                 *top_s = top;
             }
         }
-        __syncwarp();
+        __syncwarp(gmask);
         ++rows_done;
         T_last = (double)tmin;
     }
@@ -747,22 +786,47 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             const int i = r + 1;
             sm.jlo[r] = (short)(bmax >= i ? 1 : (int)(i - bmax + 1));
         }
-        // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2)
+        // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2), or the
+        // uniform baseline w_k = 1/K with T_com = max_k T_k,com (eq:ul_latency)
+        const bool uniform = C.bw_policy == SDEDGE_BW_UNIFORM;
         double tc = 0.0, q = 0.0;
         if (!bad)
             for (int k = tid; k < K; k += kThreads) {
                 const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
-                tc += C.lambda * (double)sm.I[k] / (C.Bw * sk);
-                q += (double)sm.I[k] / sk;
+                if (uniform) {
+                    const double r = (1.0 / K) * C.Bw * sk;
+                    tc = fmax(tc, C.lambda * (double)sm.I[k] / r);
+                } else {
+                    tc += C.lambda * (double)sm.I[k] / (C.Bw * sk);
+                    q += (double)sm.I[k] / sk;
+                }
             }
         for (int o = 16; o > 0; o >>= 1) {
-            tc += __shfl_xor_sync(0xffffffffu, tc, o);
+            const double ot = __shfl_xor_sync(0xffffffffu, tc, o);
+            tc = uniform ? fmax(tc, ot) : tc + ot;
             q += __shfl_xor_sync(0xffffffffu, q, o);
         }
         if (lane == 0) { sm.red[warp] = tc; sm.red[kWarps + warp] = q; }
+        // ---- fixed-plan baselines (gamma-independent): start of the batch ending at each row
+        if (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX) {
+            int b = 1;
+            if (C.batch_policy == SDEDGE_BATCH_STATIC) b = min(C.static_batch, K);
+            if (C.batch_policy == SDEDGE_BATCH_MAX) {      // largest size for the longest input (reading B4)
+                const int jl = sm.jlo[K - 1];
+                b = jl > K ? 0 : K - jl + 1;
+            }
+            for (int r = tid; r < K; r += kThreads) {
+                const int e = r + 1;
+                sm.jf[r] = b < 1 ? (short)(e == K ? -1 : 0)
+                                 : (short)((e % b == 0 || e == K) ? ((e - 1) / b) * b + 1 : 0);
+            }
+        }
         __syncthreads();
         double Tcom = 0.0, qsum = 0.0;
-        for (int w = 0; w < kWarps; ++w) { Tcom += sm.red[w]; qsum += sm.red[kWarps + w]; }
+        for (int w = 0; w < kWarps; ++w) {
+            Tcom = uniform ? fmax(Tcom, sm.red[w]) : Tcom + sm.red[w];
+            qsum += sm.red[kWarps + w];
+        }
 
         const double alpha = in.alpha[s];
         const bool bad_alpha = !(alpha > 0.0 && alpha < 1.0);
@@ -783,9 +847,41 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 const bool active = gi < ng;       // an idle group repeats gi0 without writing
                 if (!active) gi = gi0;
                 bool ovf = false;
-                const double t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v,
-                                                   active ? sm.S + (size_t)gi * K : nullptr, &ovf, wc,
-                                                   &s_top[warp * G + grp], active);
+                short* Sg = active ? sm.S + (size_t)gi * K : nullptr;
+                const short* jf = (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX)
+                                      ? sm.jf : nullptr;
+                double t;
+                if (C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
+                    // heuristic batching (reading B5): equal batches of size
+                    // 2, 3, ... in sorted order until the pipelined latency stops improving
+                    short* jw = sm.jw + (size_t)warp * K;
+                    auto plan = [&](int b) {
+                        for (int r = lane; r < K; r += 32) {
+                            const int e = r + 1;
+                            jw[r] = (short)((e % b == 0 || e == K) ? ((e - 1) / b) * b + 1 : 0);
+                        }
+                        __syncwarp();
+                    };
+                    double tb = dinf();
+                    int bb = 1;
+                    for (int b = K >= 2 ? 2 : 1; b <= K; ++b) {
+                        plan(b);
+                        const double tt = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v,
+                                                               c2v, nullptr, &ovf, wc, &s_top[warp * G + grp],
+                                                               active, jw);
+                        if (!(tt < tb) && !isinf(tb)) break;       // latency starts to degrade
+                        if (isinf(tt)) break;                      // memory binds
+                        tb = tt;
+                        bb = b;
+                    }
+                    if (isinf(tb)) bb = 1;
+                    plan(bb);
+                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v, Sg, &ovf, wc,
+                                             &s_top[warp * G + grp], active, jw);
+                } else {
+                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v, Sg, &ovf, wc,
+                                             &s_top[warp * G + grp], active, jf);
+                }
                 if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
@@ -846,7 +942,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 double wk = dnan();
                 if (!sm.ctl[3]) {
                     const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
-                    wk = ((double)Ig[k] / sk) / qsum;
+                    wk = C.bw_policy == SDEDGE_BW_UNIFORM ? 1.0 / K : ((double)Ig[k] / sk) / qsum;
                 }
                 out.w[s * K + k] = wk;
             }
@@ -906,6 +1002,12 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
     if (p->precision != 0 && p->precision != 1) return fail(-1, "precision must be 0 (fp64) or 1 (fp32)");
     if (p->algo != SDEDGE_ALGO_ENVELOPE && p->algo != SDEDGE_ALGO_DENSE) return fail(-1, "unknown algo");
     if (p->flags & ~SDEDGE_FLAG_TINY_POOL) return fail(-1, "unknown flags");
+    if (p->bandwidth_policy != SDEDGE_BW_OPTIMAL && p->bandwidth_policy != SDEDGE_BW_UNIFORM)
+        return fail(-1, "unknown bandwidth_policy");
+    if (p->batching_policy < SDEDGE_BATCH_PROPOSED || p->batching_policy > SDEDGE_BATCH_HEURISTIC)
+        return fail(-1, "unknown batching_policy");
+    if (p->batching_policy == SDEDGE_BATCH_STATIC && p->static_batch < 1) return fail(-1, "static_batch < 1");
+    if (p->reserved != 0) return fail(-1, "reserved must be 0");
     if (!(p->downlink_s >= 0) || !std::isfinite(p->downlink_s)) return fail(-1, "downlink_s must be >= 0");
     if (n > 0) {
         if (!s->input_len || !s->tx_power_w || !s->gain || !s->alpha) return fail(-1, "null scenario array");
@@ -1012,12 +1114,16 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     C.gamma_s = p->mem_capacity_bytes;
     C.Gp = (long long)C.Jd * (8LL * C.hd * C.hd + 4LL * C.hd * C.h2d);                      // eq:memory_model
     C.kvunit = 4LL * C.Jd * C.hd;                                                            // eq:memory_kv
+    C.bw_policy = p->bandwidth_policy;
+    C.batch_policy = p->batching_policy;
+    C.static_batch = p->static_batch;
     Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
     Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
                 reinterpret_cast<unsigned long long*>(o->work_counters)};
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
     // DPs per warp (envelope): 4 for small K, 2 for medium, 1 for large (r01 sweep)
-    const int G = p->algo == SDEDGE_ALGO_DENSE ? 1 : (p->K <= 48 ? 4 : p->K <= 96 ? 2 : 1);
+    const int G = (p->algo == SDEDGE_ALGO_DENSE || p->batching_policy != SDEDGE_BATCH_PROPOSED)
+                      ? 1 : (p->K <= 48 ? 4 : p->K <= 96 ? 2 : 1);
     const int f = p->flags;
     if (p->precision == 0) {
         if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<double, SDEDGE_ALGO_DENSE, 1>(C, in, out, n, st, f);

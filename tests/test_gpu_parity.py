@@ -256,3 +256,31 @@ def test_host_entry_point_chunked():
     h = to_numpy(h)
     for k in d:
         assert np.array_equal(d[k], h[k]), k
+
+
+# ---------------------------------------------------------------- paper baselines (NEXT-2)
+@pytest.mark.parametrize("pol", [1, 2, 3, 4, 5])
+def test_batching_policies(pol):
+    """SD w/o pipeline, no batching, static, max and heuristic batching
+     against the oracle."""
+    _, sc, _ = scengen.config("C3", 0, 300)
+    for pair in ("68M-7B", "1.1B-7B"):
+        pd = dict(scengen.params(pair, K=32, gamma_min=1, gamma_max=8), batching_policy=pol, static_batch=5)
+        for algo in (ENV, DENSE):
+            res, _, g = _check(pd, sc, 0, algo)
+            assert res["failures"] == 0
+    pd = dict(scengen.params("1.1B-7B", K=128, gamma_min=1, gamma_max=16), batching_policy=pol, static_batch=5)
+    _, sc4, _ = scengen.config("C4", 0, 24)
+    _check(pd, sc4, 0, ENV)
+
+
+def test_uniform_bandwidth_policy():
+    """Uniform w_k = 1/K: T_com never below the optimal t*_com,
+    T_inf and the schedule unchanged (decoupling)."""
+    pd, sc, _ = scengen.config("C3", 0, 500)
+    a = gpu_solve(pd, sc)
+    pu = dict(pd, bandwidth_policy=1)
+    res, _, b = _check(pu, sc, 0, ENV)
+    assert np.all(b["lat"][:, 1] >= a["lat"][:, 1] * (1 - 1e-12))
+    assert np.array_equal(a["lat"][:, 2], b["lat"][:, 2]) and np.array_equal(a["batch_end"], b["batch_end"])
+    assert np.all(b["w"] == 1.0 / 32)

@@ -1,0 +1,130 @@
+"""Pins for the oracle's paper-baseline policies (Sec. IV, P:818-826, P:903-911,
+P:936-940), -m "not gpu".  SURVEY.md 8(f) NEXT-2."""
+import math
+
+import numpy as np
+import pytest
+
+import scengen
+
+BW_UNIFORM = 1
+NO_PIPE, NONE, STATIC, MAX, HEUR = 1, 2, 3, 4, 5
+
+
+def rel(a, b):
+    return abs(a - b) / abs(b)
+
+
+def test_uniform_bandwidth_spec_example(orc):
+    """uniform shares on the two-task example give max(lam 100 2 /(B 10),
+    lam 300 2 /(B 5)) = lam 120 / B, strictly above t* = lam 70 / B."""
+    pd = scengen.params("1.1B-7B", K=2, noise_w=1.0)
+    lam, B = 98304, 20e6
+    t_opt, _ = orc.bandwidth(pd, [100, 300], [1.0, 1.0], [1023.0, 31.0])
+    t_uni, w = orc.bandwidth(dict(pd, bandwidth_policy=BW_UNIFORM), [100, 300], [1.0, 1.0], [1023.0, 31.0])
+    assert rel(t_uni, lam * 120 / B) < 1e-14 and t_uni > t_opt
+    assert list(w) == [0.5, 0.5]
+
+
+def test_uniform_never_better_and_equal_when_symmetric(orc):
+    rng = np.random.default_rng(31)
+    pd = scengen.params("68M-7B", K=12)
+    for _ in range(40):
+        sc = scengen.generate(int(rng.integers(1 << 30)), 12, 0, 1)
+        t_opt, _ = orc.bandwidth(pd, sc["I"][0], sc["p"][0], sc["g"][0])
+        t_uni, _ = orc.bandwidth(dict(pd, bandwidth_policy=BW_UNIFORM), sc["I"][0], sc["p"][0], sc["g"][0])
+        assert t_uni >= t_opt * (1 - 1e-12)
+    # identical tasks: both schemes coincide (w* = 1/K)
+    t_opt, _ = orc.bandwidth(pd, [100] * 12, [0.2] * 12, [1e-8] * 12)
+    t_uni, _ = orc.bandwidth(dict(pd, bandwidth_policy=BW_UNIFORM), [100] * 12, [0.2] * 12, [1e-8] * 12)
+    assert rel(t_uni, t_opt) < 1e-12
+
+
+def test_nopipe_dp_is_exact(orc):
+    """The SD-w/o-pipeline cost is additive over batches, so Algorithm 1's
+    recursion is exact for it: equals brute force over contiguous partitions."""
+    rng = np.random.default_rng(32)
+    for K in (1, 2, 4, 6):
+        for _ in range(6):
+            pair = ["68M-7B", "1.1B-7B", "1.1B-13B"][int(rng.integers(3))]
+            pd = scengen.params(pair, K=K, O_max=int(rng.choice([32, 300])))
+            Is = np.sort(rng.integers(1, 513, K)).astype(np.int32)
+            a = float(rng.uniform(0.5, 0.9))
+            for g in (0, 2, 7):
+                t, S, gap, W = orc.dp_nopipe(pd, Is, a, g)
+                plan = orc.backtrack(S)
+                assert rel(orc.eval_plan_nopipe(pd, Is, a, g, plan), t) < 1e-12
+                best = math.inf
+                for mask in range(1 << (K - 1)):
+                    ends = [t_ + 1 for t_ in range(K - 1) if mask >> t_ & 1] + [K]
+                    best = min(best, orc.eval_plan_nopipe(pd, Is, a, g, ends))
+                assert rel(t, best) < 1e-12
+
+
+def test_pipelining_dominance(orc):
+    """For every plan, each step's pipelined makespan <= the sequential sum
+    (P:505-517 vs P:820), with equality for a single batch."""
+    rng = np.random.default_rng(33)
+    pd = scengen.params("1.1B-13B", K=6, O_max=100)
+    for _ in range(20):
+        Is = np.sort(rng.integers(1, 513, 6)).astype(np.int32)
+        a = float(rng.uniform(0.5, 0.9))
+        g = int(rng.integers(0, 9))
+        cuts = sorted(rng.choice(np.arange(1, 6), size=int(rng.integers(0, 5)), replace=False).tolist())
+        ends = cuts + [6]
+        assert orc.eval_plan(pd, Is, a, g, ends) <= orc.eval_plan_nopipe(pd, Is, a, g, ends) * (1 + 1e-12)
+        assert rel(orc.eval_plan(pd, Is, a, g, [6]), orc.eval_plan_nopipe(pd, Is, a, g, [6])) < 1e-12
+
+
+def test_fixed_plans(orc):
+    Is = np.sort(np.random.default_rng(34).integers(1, 513, 13)).astype(np.int32)
+    pd = scengen.params("68M-7B", K=13, O_max=64)
+    assert orc.fixed_plan(dict(pd, batching_policy=NONE), Is, 0.7, 3) == list(range(1, 14))
+    assert orc.fixed_plan(dict(pd, batching_policy=STATIC, static_batch=4), Is, 0.7, 3) == [4, 8, 12, 13]
+    assert orc.fixed_plan(dict(pd, batching_policy=STATIC, static_batch=40), Is, 0.7, 3) == [13]
+    # max batching: 68M never binds (b = K); 1.1B binds at 30 for I = 512
+    assert orc.fixed_plan(dict(pd, batching_policy=MAX), Is, 0.7, 3) == [13]
+    pd11 = scengen.params("1.1B-7B", K=70)
+    Is512 = np.full(70, 512, np.int32)
+    assert orc.fixed_plan(dict(pd11, batching_policy=MAX), Is512, 0.7, 3) == [30, 60, 70]
+    assert orc.fixed_plan(dict(pd11, batching_policy=MAX, mem_capacity_bytes=10**9), Is512, 0.7, 3) == []
+
+
+def test_heuristic_stopping_rule(orc):
+    """Heuristic batching (reading B5): sizes 2, 3, ... while the pipelined
+    latency (eq:time) keeps improving; the returned size is the last improving
+    one -- checked against eval_plan of every equal-size plan."""
+    rng = np.random.default_rng(35)
+    for _ in range(25):
+        K = int(rng.integers(2, 24))
+        pair = ["68M-7B", "1.1B-7B"][int(rng.integers(2))]
+        pd = dict(scengen.params(pair, K=K, O_max=int(rng.choice([64, 512]))), batching_policy=HEUR)
+        Is = np.sort(rng.integers(1, 513, K)).astype(np.int32)
+        a = float(rng.uniform(0.5, 0.9))
+        g = int(rng.integers(1, 9))
+        ends = orc.fixed_plan(pd, Is, a, g)
+
+        def plan(b):
+            return [e for e in range(b, K, b)] + [K]
+        T = {b: orc.eval_plan(pd, Is, a, g, plan(b)) for b in range(2, K + 1)}
+        b = 2
+        while b + 1 <= K and T[b + 1] < T[b]:
+            b += 1
+        assert ends == plan(b)
+
+
+def test_policy_solves_are_consistent(orc):
+    """Every policy's T_inf equals the literal evaluation of its own plan and
+    gamma; FSL is gamma_min = gamma_max = 7; ADS core is gamma = 0."""
+    _, sc, _ = scengen.config("C3", 0, 6)
+    for pol in (NO_PIPE, NONE, STATIC, MAX, HEUR):
+        pd = dict(scengen.params("1.1B-7B", K=32, gamma_min=1, gamma_max=8), batching_policy=pol)
+        out = orc.solve_batch(pd, sc)
+        for s in range(6):
+            assert out["status"][s] == 0
+            Is = sc["I"][s][out["order"][s]]
+            ends = list(out["batch_end"][s][: out["M"][s]])
+            ev = orc.eval_plan_nopipe if pol == NO_PIPE else orc.eval_plan
+            assert rel(ev(pd, Is, float(sc["alpha"][s]), int(out["gamma"][s]), ends), out["lat"][s, 2]) < 1e-12
+    fsl = orc.solve_batch(scengen.params("68M-7B", K=32, gamma_min=7, gamma_max=7), sc)
+    assert np.all(fsl["gamma"] == 7)
