@@ -140,6 +140,20 @@ int sdedge_solve_batch(const sdedge_scenarios* scenarios, int64_t n, const sdedg
 int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
                             double* out_latency, sdedge_schedule* out_schedule);
 
+/* Actual-output evaluation of solved schedules (P:316-318,
+ * eq:step_n, eq:latency_infer_batch P:519-525, eq:latency_inf).  The planner
+ * assumes O_k = O_max; this call replays each scenario's plan
+ * (gamma, batch_end, order from sdedge_solve_batch) with the tasks' actual
+ * output lengths: batch m runs n_m = ceil(O_m / L) steps, O_m = max of its
+ * tasks' O_k, and at step n only batches with n_m >= n go through eq:time.
+ * output_len: DEVICE [n*K] int32 >= 1 (original task order); plan: DEVICE
+ * arrays gamma, num_batches, batch_end, order, status (others ignored);
+ * out_t_inf: DEVICE [n] actual T_inf in seconds (NaN where status != 0 or
+ * some O_k < 1).  Uses the same params (models, coefficients, K, O_max,
+ * stream) as the solve.  Asynchronous; returns 0 / -1 / -2 like the solve. */
+int sdedge_evaluate_actual(const sdedge_scenarios* scenarios, const int32_t* output_len, int64_t n,
+                           const sdedge_params* params, const sdedge_schedule* plan, double* out_t_inf);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int sdedge_last_launch_count(void);
 

@@ -85,6 +85,8 @@ def lib():
         L.orc_dp_nopipe.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_f64, P_i64]
         L.orc_fixed_plan.restype = C.c_int
         L.orc_fixed_plan.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32]
+        L.orc_eval_actual.restype = C.c_double
+        L.orc_eval_actual.argtypes = [C.POINTER(Params), P_f64, P_i32, P_i32, C.c_double, C.c_int, C.c_int, P_i32]
         L.orc_solve.restype = None
         L.orc_solve.argtypes = [C.POINTER(Params), P_i32, P_f64, P_f64, C.c_double, P_f64,
                                 C.POINTER(Result), P_i32, P_i32, P_f64, P_f64]
@@ -201,6 +203,17 @@ def eval_plan_nopipe(pd, Is, alpha, gamma, batch_end, coeffs=None):
     co = _co(coeffs)
     return lib().orc_eval_plan_nopipe(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma,
                                       len(be), _p(be, C.c_int32))
+
+
+def eval_actual(pd, Is, Os, alpha, gamma, batch_end, coeffs=None):
+    """Actual-output evaluation of a plan (Is, Os in sorted order)."""
+    P = make_params(dict(pd, K=len(Is)))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    Os = np.ascontiguousarray(Os, dtype=np.int32)
+    be = np.ascontiguousarray(batch_end, dtype=np.int32)
+    co = _co(coeffs)
+    return lib().orc_eval_actual(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), _p(Os, C.c_int32), alpha,
+                                 gamma, len(be), _p(be, C.c_int32))
 
 
 def dp_nopipe(pd, Is, alpha, gamma, coeffs=None):

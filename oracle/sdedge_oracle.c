@@ -172,6 +172,37 @@ double orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, d
     return Tinf;
 }
 
+double orc_eval_actual(const orc_params* P, const double* co, const int32_t* Is, const int32_t* Os,
+                       double alpha, int gamma, int M, const int32_t* batch_end)
+{
+    double L = orc_expected_tokens(alpha, gamma);
+    int* nm = (int*)malloc(sizeof(int) * (M > 0 ? M : 1));
+    int N = 0;
+    for (int m = 0; m < M; ++m) {
+        int start = m ? batch_end[m - 1] + 1 : 1;
+        int Om = 0;                                   /* O_m = max_k x_k^m O_k */
+        for (int q = start; q <= batch_end[m]; ++q) if (Os[q - 1] > Om) Om = Os[q - 1];
+        nm[m] = orc_decode_steps(Om, L);              /* eq:step_n */
+        if (nm[m] > N) N = nm[m];                     /* N = max_m n_m */
+    }
+    double Tinf = 0.0;
+    for (int n = 1; n <= N; ++n) {
+        double Cd = 0.0, C = 0.0;
+        for (int m = 0; m < M; ++m) {
+            if (nm[m] < n) continue;                  /* active set M_n */
+            int start = m ? batch_end[m - 1] + 1 : 1;
+            int b = batch_end[m] - start + 1;
+            int32_t Im = Is[batch_end[m] - 1];
+            Cd += orc_draft_time(P, co, b, Im, gamma, L, n);
+            double st = Cd > C ? Cd : C;
+            C = st + orc_verify_time(P, co, b, Im, gamma, L, n);
+        }
+        Tinf += C;                                    /* T_n = C_{n, M_n} */
+    }
+    free(nm);
+    return Tinf;
+}
+
 double orc_eval_plan_nopipe(const orc_params* P, const double* co, const int32_t* Is, double alpha,
                             int gamma, int M, const int32_t* batch_end)
 {

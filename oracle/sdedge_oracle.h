@@ -92,6 +92,14 @@ double  orc_dp_nopipe(const orc_params* P, const double* co, const int32_t* Is, 
 int     orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
                        int32_t* ends);
 
+/* Actual-output evaluation of a plan (eq:step_n, eq:latency_infer_batch
+ * P:519-525, eq:latency_inf): batch m needs n_m = ceil(O_m / L) steps with O_m the
+ * largest actual output length O_k of its tasks; at step n only the batches with
+ * n_m >= n run, in plan order, through the eq:time recursion.
+ * Is: sorted input lengths; Os: the actual output lengths in the same sorted order. */
+double  orc_eval_actual(const orc_params* P, const double* co, const int32_t* Is, const int32_t* Os,
+                        double alpha, int gamma, int M, const int32_t* batch_end);
+
 /* Full solve of problem P for one scenario.
  * order[K], batch_end[K], w[K], tinf_gamma[gamma_max-gamma_min+1] are caller-owned. */
 void    orc_solve(const orc_params* P, const int32_t* I, const double* p, const double* g,

@@ -12,7 +12,7 @@ import os
 
 from ._build import LIB, build  # noqa: F401
 
-__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_pipe_peak", "sdedge_last_error",
+__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual", "evaluate_actual", "sdedge_pipe_peak", "sdedge_last_error",
            "sdedge_last_launch_count", "sdedge_abi_version", "solve", "solve_host", "make_params",
            "ALGO_ENVELOPE", "ALGO_DENSE", "EXPORTED_SYMBOLS", "lib"]
 
@@ -20,8 +20,8 @@ ALGO_ENVELOPE, ALGO_DENSE = 0, 1
 BW_OPTIMAL, BW_UNIFORM = 0, 1
 BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC = range(6)
 FLAG_TINY_POOL = 1
-EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_last_launch_count",
-                    "sdedge_last_error", "sdedge_abi_version", "sdedge_pipe_peak")
+EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
+                    "sdedge_last_launch_count", "sdedge_last_error", "sdedge_abi_version", "sdedge_pipe_peak")
 
 
 class SdedgeModel(C.Structure):
@@ -67,6 +67,9 @@ def lib() -> C.CDLL:
             fn.restype = C.c_int
             fn.argtypes = [C.POINTER(SdedgeScenarios), C.c_int64, C.POINTER(SdedgeParams), C.c_void_p,
                            C.POINTER(SdedgeSchedule)]
+        L.sdedge_evaluate_actual.restype = C.c_int
+        L.sdedge_evaluate_actual.argtypes = [C.POINTER(SdedgeScenarios), C.c_void_p, C.c_int64,
+                                             C.POINTER(SdedgeParams), C.POINTER(SdedgeSchedule), C.c_void_p]
         L.sdedge_last_error.restype = C.c_char_p
         L.sdedge_last_launch_count.restype = C.c_int
         L.sdedge_abi_version.restype = C.c_int
@@ -132,6 +135,31 @@ def sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, params: SdedgeParams, out
     """Direct C-ABI call on HOST buffers (numpy or pinned torch CPU tensors)."""
     return _call(lib().sdedge_solve_batch_host, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
                  num_batches, batch_end, order, bw_share, status)
+
+
+def sdedge_evaluate_actual(I, p, g, alpha, coeffs, output_len, n, params: SdedgeParams, gamma, num_batches,
+                           batch_end, order, status, out_t_inf):
+    """Direct C-ABI call (DEVICE tensors): actual-output T_inf of solved plans."""
+    sc = SdedgeScenarios(_ptr(I), _ptr(p), _ptr(g), _ptr(alpha), _ptr(coeffs))
+    sch = SdedgeSchedule(_ptr(gamma), _ptr(num_batches), _ptr(batch_end), _ptr(order), None, _ptr(status), None)
+    rc = lib().sdedge_evaluate_actual(C.byref(sc), _ptr(output_len), n, C.byref(params), C.byref(sch),
+                                      _ptr(out_t_inf))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_evaluate_actual failed ({rc}): {sdedge_last_error()}")
+    return rc
+
+
+def evaluate_actual(params: dict, I, p, g, alpha, output_len, plan: dict, coeffs=None, stream=None):
+    """Actual-output T_inf [n] (CUDA tensor) of the plans in `plan` (solve() output)."""
+    import torch
+    n, K = I.shape
+    if stream is None:
+        stream = torch.cuda.current_stream(I.device)
+    P = make_params(dict(params, K=K), stream=stream)
+    out = torch.empty(n, dtype=torch.float64, device=I.device)
+    sdedge_evaluate_actual(I, p, g, alpha, coeffs, output_len, n, P, plan["gamma"], plan["M"], plan["batch_end"],
+                           plan["order"], plan["status"], out)
+    return out
 
 
 def sdedge_pipe_peak(fp32: bool = False):

@@ -959,6 +959,99 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     }
 }
 
+// ------------------------------------------------------------ actual-output evaluation
+// One warp per scenario (grid-stride).  Per batch: b_m, padded I_m and the
+// closed-form stage coefficients (D1) go to shared memory with
+// n_m = ceil(O_m / L) (exact IEEE sequence, reading A2); lanes then take steps
+// n and run the eq:time recursion over the batches still active at n.
+struct ActBatch {
+    double td1, ad, bd, tv1, av, bv;   // T^d_1, T^d_n = ad + bd (n-1); T^v likewise (already x b, + c2)
+    int nm, pad;
+};
+
+__global__ void __launch_bounds__(128)
+actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, const int32_t* __restrict__ gam,
+              const int32_t* __restrict__ Mv, const int32_t* __restrict__ bend, const int32_t* __restrict__ order,
+              const int32_t* __restrict__ status, long long n, double* __restrict__ out)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = C.K, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    ActBatch* bt = reinterpret_cast<ActBatch*>(smem_raw) + (size_t)warp * K;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + warp; s < n; s += nw) {
+        const int M = Mv[s];
+        const int g = gam[s];
+        if (status[s] != 0 || M < 1 || M > K) {
+            if (lane == 0) out[s] = dnan();
+            continue;
+        }
+        const double alpha = in.alpha[s];
+        double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
+        if (in.coeffs) {
+            c1d = in.coeffs[4 * s]; c2d = in.coeffs[4 * s + 1];
+            c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
+        }
+        const double L = expected_tokens(alpha, g);
+        DPConst D;
+        D.g = g;
+        D.tri = D.g * (D.g - 1.0) * 0.5;
+        D.kd = c1d * (4.0 * C.Jd * (double)C.hd);
+        D.kv = c1v * (4.0 * C.Jv * (double)C.hv);
+        D.hd2 = 2.0 * C.hd + C.h2d;
+        D.hv2 = 2.0 * C.hv + C.h2v;
+        D.bdc = D.kd * D.g * L;
+        D.bvc = D.kv * (1.0 + D.g) * L;
+        D.c2dg = D.g * c2d;
+        D.c2vv = c2v + C.dl;
+        D.Mx = 0.0;
+        D.sumM = 0.0;
+        int nmax = 0, bad = 0;
+        for (int m = lane; m < M; m += 32) {
+            const int e = bend[s * K + m], st = m ? bend[s * K + m - 1] + 1 : 1;
+            int Om = 0;
+            for (int q = st; q <= e; ++q) {
+                const int o = O[s * K + order[s * K + q - 1]];
+                Om = max(Om, o);
+                bad |= o < 1;
+            }
+            const int I = in.I[s * K + order[s * K + e - 1]];
+            const RowCoef rc = row_coef(D, I);
+            const double b = e - st + 1;
+            ActBatch a;
+            a.td1 = fma(b, rc.td1, D.c2dg);
+            a.ad = fma(b, rc.ad, D.c2dg);
+            a.bd = b * D.bdc;
+            a.tv1 = fma(b, rc.tv1, D.c2vv);
+            a.av = fma(b, rc.av, D.c2vv);
+            a.bv = b * D.bvc;
+            a.nm = (int)ceil(__ddiv_rn((double)Om, L));   // eq:step_n
+            a.pad = 0;
+            bt[m] = a;
+            nmax = max(nmax, a.nm);
+        }
+        nmax = __reduce_max_sync(0xffffffffu, nmax);
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        __syncwarp();
+        double acc = 0.0;
+        for (int step = 1 + lane; step <= nmax; step += 32) {
+            const double x = step - 1;
+            double Cd = 0.0, Cc = 0.0;
+            for (int m = 0; m < M; ++m) {
+                const ActBatch a = bt[m];
+                if (a.nm < step) continue;                // M_n
+                const double td = step == 1 ? a.td1 : fma(a.bd, x, a.ad);
+                const double tv = step == 1 ? a.tv1 : fma(a.bv, x, a.av);
+                Cd += td;                                 // C^d_{n,m}
+                Cc = rmax(Cd, Cc) + tv;                   // eq:time
+            }
+            acc += Cc;                                    // T_n = C_{n, M_n}
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[s] = bad ? dnan() : acc;
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------ pipe-peak microbenchmark
 template <typename T>
 __global__ void pipe_peak_kernel(T* sink, int iters, T seed)
@@ -1100,8 +1193,7 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     return 0;
 }
 
-int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* lat,
-                 sdedge_schedule* o)
+Consts make_consts(const sdedge_params* p)
 {
     Consts C{};
     C.K = p->K; C.O_max = p->O_max; C.gmin = p->gamma_min; C.ng = p->gamma_max - p->gamma_min + 1;
@@ -1117,6 +1209,13 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     C.bw_policy = p->bandwidth_policy;
     C.batch_policy = p->batching_policy;
     C.static_batch = p->static_batch;
+    return C;
+}
+
+int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* lat,
+                 sdedge_schedule* o)
+{
+    Consts C = make_consts(p);
     Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
     Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
                 reinterpret_cast<unsigned long long*>(o->work_counters)};
@@ -1236,6 +1335,40 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     for (int q = 0; q < 2; ++q) CU(cudaStreamDestroy(ss[q]));   // released once their work drains
     for (int q = 0; q < 3; ++q) CU(cudaEventDestroy(ev[q]));
     g_launches = launches;
+    return 0;
+}
+
+int sdedge_evaluate_actual(const sdedge_scenarios* s, const int32_t* output_len, int64_t n, const sdedge_params* p,
+                           const sdedge_schedule* plan, double* out_t_inf)
+{
+    g_err[0] = 0;
+    g_launches = 0;
+    sdedge_schedule dummy{};
+    int rc = validate(s, 0, p, nullptr, &dummy);
+    if (rc) return rc;
+    if (n < 0) return fail(-1, "n < 0");
+    if (n == 0) return 0;
+    if (!s->input_len || !s->alpha || !output_len || !plan || !plan->gamma || !plan->num_batches ||
+        !plan->batch_end || !plan->order || !plan->status || !out_t_inf)
+        return fail(-1, "null argument");
+    Consts C = make_consts(p);
+    Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
+    int dev = 0, nsm = 0, max_smem = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int warps = 4;
+    while (warps > 1 && (size_t)warps * C.K * sizeof(ActBatch) > 96 * 1024) warps >>= 1;
+    const size_t sb = (size_t)warps * C.K * sizeof(ActBatch);
+    if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
+    CU(cudaFuncSetAttribute(actual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    long long blocks = std::min<long long>((n + warps - 1) / warps, (long long)nsm * 16);
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    actual_kernel<<<(unsigned)blocks, warps * 32, sb, st>>>(C, in, output_len, plan->gamma, plan->num_batches,
+                                                           plan->batch_end, plan->order, plan->status, n,
+                                                           out_t_inf);
+    CU(cudaGetLastError());
+    g_launches = 1;
     return 0;
 }
 

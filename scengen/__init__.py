@@ -114,6 +114,14 @@ def generate(root: int, K: int, s0: int, s1: int, I_max: int = 512,
                 alpha=np.ascontiguousarray(alpha), coeffs=None)
 
 
+def output_lengths(root: int, K: int, s0: int, s1: int, O_max: int = 2048) -> np.ndarray:
+    """Actual output lengths O_k uniform on {1..O_max}, counter c = 1 + 3K + k
+    (after the task draws), for the actual-output evaluation."""
+    s = np.arange(s0, s1, dtype=np.uint64)[:, None]
+    k = np.arange(K, dtype=np.uint64)[None, :]
+    return np.ascontiguousarray((1 + np.floor(O_max * _u01(u64(root, s, 1 + 3 * K + k)))).astype(np.int32))
+
+
 # ---------------------------------------------------------------- configs
 # SURVEY.md Sec. 8(d) table; BASELINE.json "configs".
 GOLDEN_C1 = dict(I=[512, 37, 255, 100], g=[1e-8, 4e-9, 2.5e-8, 1e-9], alpha=0.8)

@@ -284,3 +284,36 @@ def test_uniform_bandwidth_policy():
     assert np.all(b["lat"][:, 1] >= a["lat"][:, 1] * (1 - 1e-12))
     assert np.array_equal(a["lat"][:, 2], b["lat"][:, 2]) and np.array_equal(a["batch_end"], b["batch_end"])
     assert np.all(b["w"] == 1.0 / 32)
+
+
+# ---------------------------------------------------------------- actual outputs (NEXT-1)
+@pytest.mark.parametrize("cfg,pair,n", [("C3", "68M-7B", 2000), ("C3", "1.1B-7B", 2000), ("C2", None, 3),
+                                        ("C4", "68M-7B", 64)])
+def test_actual_output_evaluation(cfg, pair, n):
+    """sdedge_evaluate_actual on the GPU's own plans vs the oracle's literal
+    replay (eq:step_n, M_n, eq:time) of the same plans with O_k ~ U{1..O_max}."""
+    import paper_2510_11331_b200 as sd
+    pd, sc, _ = scengen.config(cfg, 0, n, pair=pair)
+    K = pd["K"]
+    O = scengen.output_lengths(9, K, 0, n, pd["O_max"])
+    dev = "cuda:0"
+    t = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).to(dev) for k in ("I", "p", "g", "alpha")}
+    co = None if sc.get("coeffs") is None else torch.from_numpy(sc["coeffs"]).to(dev)
+    plan = sd.solve(pd, t["I"], t["p"], t["g"], t["alpha"], co)
+    act = sd.evaluate_actual(pd, t["I"], t["p"], t["g"], t["alpha"], torch.from_numpy(O).to(dev), plan, co)
+    torch.cuda.synchronize()
+    act = act.cpu().numpy()
+    pl = to_numpy(plan)
+    for s in range(n):
+        Is = sc["I"][s][pl["order"][s]]
+        Os = O[s][pl["order"][s]]
+        ends = list(pl["batch_end"][s][: pl["M"][s]])
+        cs = None if sc.get("coeffs") is None else sc["coeffs"][s]
+        v = oracle.eval_actual(pd, Is, Os, float(sc["alpha"][s]), int(pl["gamma"][s]), ends, coeffs=cs)
+        assert abs(act[s] - v) <= 1e-12 * v, (s, act[s], v)
+        assert act[s] <= pl["lat"][s, 2] * (1 + 1e-12)
+    # O_k = O_max reproduces the planned T_inf
+    full = sd.evaluate_actual(pd, t["I"], t["p"], t["g"], t["alpha"],
+                              torch.full((n, K), pd["O_max"], dtype=torch.int32, device=dev), plan, co)
+    torch.cuda.synchronize()
+    assert np.allclose(full.cpu().numpy(), pl["lat"][:, 2], rtol=1e-12, atol=0)

@@ -128,3 +128,32 @@ def test_policy_solves_are_consistent(orc):
             assert rel(ev(pd, Is, float(sc["alpha"][s]), int(out["gamma"][s]), ends), out["lat"][s, 2]) < 1e-12
     fsl = orc.solve_batch(scengen.params("68M-7B", K=32, gamma_min=7, gamma_max=7), sc)
     assert np.all(fsl["gamma"] == 7)
+
+
+# ---------------------------------------------------------------- NEXT-1
+def test_actual_output_evaluation(orc):
+    """Actual-output evaluation: equals the planned
+    evaluation when every O_k = O_max, never exceeds it, and a batch that has
+    finished drops out of later steps."""
+    rng = np.random.default_rng(36)
+    pd = scengen.params("1.1B-7B", K=9, O_max=300)
+    for _ in range(20):
+        Is = np.sort(rng.integers(1, 513, 9)).astype(np.int32)
+        Os = rng.integers(1, 301, 9).astype(np.int32)
+        a = float(rng.uniform(0.5, 0.9))
+        g = int(rng.integers(0, 9))
+        cuts = sorted(rng.choice(np.arange(1, 9), size=int(rng.integers(0, 8)), replace=False).tolist())
+        ends = cuts + [9]
+        full = orc.eval_plan(pd, Is, a, g, ends)
+        assert rel(orc.eval_actual(pd, Is, np.full(9, 300, np.int32), a, g, ends), full) < 1e-14
+        assert orc.eval_actual(pd, Is, Os, a, g, ends) <= full * (1 + 1e-12)
+    # two batches, n_1 = 2 and n_2 = 1: step 2 runs batch 1 alone
+    pd2 = scengen.params("68M-7B", K=2, O_max=8)
+    Is, a, g = np.array([100, 200], np.int32), 0.5, 1          # L = 1.5
+    Os = np.array([3, 1], np.int32)                              # n = ceil(3/1.5) = 2, ceil(1/1.5) = 1
+    L = orc.expected_tokens(a, g)
+    td = [[orc.draft_time(pd2, 1, int(Is[m]), g, L, n) for m in range(2)] for n in (1, 2)]
+    tv = [[orc.verify_time(pd2, 1, int(Is[m]), g, L, n) for m in range(2)] for n in (1, 2)]
+    step1 = max(td[0][0] + td[0][1], td[0][0] + tv[0][0]) + tv[0][1]
+    step2 = td[1][0] + tv[1][0]
+    assert rel(orc.eval_actual(pd2, Is, Os, a, g, [1, 2]), step1 + step2) < 1e-14
