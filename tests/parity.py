@@ -66,8 +66,8 @@ def compare(pd: dict, sc: dict, gpu: dict, orc: dict, precision: int = 0, orc_mo
                 Is = sc["I"][s][gpu["order"][s]]
                 co = None if sc.get("coeffs") is None else sc["coeffs"][s]
                 ends = list(gpu["batch_end"][s][: gpu["M"][s]])
-                v = orc_mod.eval_plan(dict(pd, K=K), Is, float(sc["alpha"][s]), int(gpu["gamma"][s]), ends,
-                                      coeffs=co)
+                ev = orc_mod.eval_plan_nopipe if pd.get("batching_policy", 0) == 1 else orc_mod.eval_plan
+                v = ev(dict(pd, K=K), Is, float(sc["alpha"][s]), int(gpu["gamma"][s]), ends, coeffs=co)
                 if abs(v - lg[2]) > 1e-12 * abs(v) or lg[2] > lo[2] * (1 + 1e-6):
                     fails.append(f"s={s}: exempt scenario not self-consistent ({v} vs {lg[2]})")
             continue
