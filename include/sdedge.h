@@ -145,7 +145,8 @@ int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const 
  * assumes O_k = O_max; this call replays each scenario's plan
  * (gamma, batch_end, order from sdedge_solve_batch) with the tasks' actual
  * output lengths: batch m runs n_m = ceil(O_m / L) steps, O_m = max of its
- * tasks' O_k, and at step n only batches with n_m >= n go through eq:time.
+ * tasks' O_k, and at step n only batches with n_m >= n go through eq:time
+ * (or, under SDEDGE_BATCH_NO_PIPELINE, run draft then verify sequentially).
  * output_len: DEVICE [n*K] int32 >= 1 (original task order); plan: DEVICE
  * arrays gamma, num_batches, batch_end, order, status (others ignored);
  * out_t_inf: DEVICE [n] actual T_inf in seconds (NaN where status != 0 or

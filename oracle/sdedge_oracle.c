@@ -193,6 +193,10 @@ double orc_eval_actual(const orc_params* P, const double* co, const int32_t* Is,
             int start = m ? batch_end[m - 1] + 1 : 1;
             int b = batch_end[m] - start + 1;
             int32_t Im = Is[batch_end[m] - 1];
+            if (P->batch_policy == 1) {               /* SD w/o pipeline: sequential stages */
+                C += orc_draft_time(P, co, b, Im, gamma, L, n) + orc_verify_time(P, co, b, Im, gamma, L, n);
+                continue;
+            }
             Cd += orc_draft_time(P, co, b, Im, gamma, L, n);
             double st = Cd > C ? Cd : C;
             C = st + orc_verify_time(P, co, b, Im, gamma, L, n);

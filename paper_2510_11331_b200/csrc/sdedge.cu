@@ -1041,6 +1041,7 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
                 if (a.nm < step) continue;                // M_n
                 const double td = step == 1 ? a.td1 : fma(a.bd, x, a.ad);
                 const double tv = step == 1 ? a.tv1 : fma(a.bv, x, a.av);
+                if (C.batch_policy == SDEDGE_BATCH_NO_PIPELINE) { Cc += td + tv; continue; }  // sequential
                 Cd += td;                                 // C^d_{n,m}
                 Cc = rmax(Cd, Cc) + tv;                   // eq:time
             }

@@ -1,3 +1,7 @@
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --algo dense --n 20000 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dense', round(d['value']), d['roofline']['frac'])"
-timeout 300 python bench.py --algo dense --config C3 --n 20000 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dense C3', round(d['value']), d['roofline']['frac'])"
+timeout 900 python tools/paper_context.py --n 2000 > gpurun_out/r01_paper_context.json 2> gpurun_out/paper_context.err; echo rc=$?
+python -c "
+import json; d=json.load(open('gpurun_out/r01_paper_context.json'))
+for k,v in d.items():
+    if isinstance(v, dict) and 'paper_pct' in v: print(f'{k:45s} paper {v[\"paper_pct\"]}  planned {v[\"planned_pct\"]:.1f}  actual {v[\"actual_pct\"]:.1f}')
+"

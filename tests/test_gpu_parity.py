@@ -287,13 +287,15 @@ def test_uniform_bandwidth_policy():
 
 
 # ---------------------------------------------------------------- actual outputs (NEXT-1)
+@pytest.mark.parametrize("pol", [0, 1])
 @pytest.mark.parametrize("cfg,pair,n", [("C3", "68M-7B", 2000), ("C3", "1.1B-7B", 2000), ("C2", None, 3),
                                         ("C4", "68M-7B", 64)])
-def test_actual_output_evaluation(cfg, pair, n):
+def test_actual_output_evaluation(cfg, pair, n, pol):
     """sdedge_evaluate_actual on the GPU's own plans vs the oracle's literal
     replay (eq:step_n, M_n, eq:time) of the same plans with O_k ~ U{1..O_max}."""
     import paper_2510_11331_b200 as sd
     pd, sc, _ = scengen.config(cfg, 0, n, pair=pair)
+    pd = dict(pd, batching_policy=pol)
     K = pd["K"]
     O = scengen.output_lengths(9, K, 0, n, pd["O_max"])
     dev = "cuda:0"

@@ -157,3 +157,16 @@ def test_actual_output_evaluation(orc):
     step1 = max(td[0][0] + td[0][1], td[0][0] + tv[0][0]) + tv[0][1]
     step2 = td[1][0] + tv[1][0]
     assert rel(orc.eval_actual(pd2, Is, Os, a, g, [1, 2]), step1 + step2) < 1e-14
+
+
+def test_actual_output_nopipe(orc):
+    """Under SD w/o pipeline the actual-output replay is sequential too, and
+    equals the sequential planned evaluation when every O_k = O_max."""
+    rng = np.random.default_rng(37)
+    pd = dict(scengen.params("1.1B-7B", K=7, O_max=200), batching_policy=NO_PIPE)
+    for _ in range(10):
+        Is = np.sort(rng.integers(1, 513, 7)).astype(np.int32)
+        a, g = float(rng.uniform(0.5, 0.9)), int(rng.integers(0, 9))
+        ends = [2, 5, 7]
+        assert rel(orc.eval_actual(pd, Is, np.full(7, 200, np.int32), a, g, ends),
+                   orc.eval_plan_nopipe(pd, Is, a, g, ends)) < 1e-14
