@@ -47,6 +47,12 @@ FP32_LANES_PER_SM = 128
 OPS = {"dense": dict(cand=16, seg=0, step=4, row=40),
        "envelope": dict(cand=16, seg=10, step=0, row=40)}
 
+# DRAM bytes (read + write) per scenario of the envelope kernel from the one
+# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_c4.md: 268.3 MB
+# read + 182.1 MB written for a 1e5-scenario C4 launch), scaled to the launch.
+# The algorithmic bytes are 2568 in + 2084 out per scenario.
+NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (268.348928e6 + 182.146304e6) / 1e5}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -341,7 +347,12 @@ def main():
             "config": cfg,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "T fp64-lane-ops/s" if prec == 0 else "T fp32-lane-ops/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": (NCU_DRAM_BYTES_PER_SCENARIO[(args.config, args.algo, args.precision)] * n
+                                     if (args.config, args.algo, args.precision) in NCU_DRAM_BYTES_PER_SCENARIO
+                                     else None),
+                         "traffic_unit": "DRAM bytes per launch (r01 ncu capture, per-scenario scaled)",
+                         "algorithmic_bytes": (20 * K + 8 + 36 + 16 * K) * n,
                          "peak_source": f"derived: {nsm} SMs x {lanes} lanes x 1965 MHz (B200_PROFILING.md)",
                          "work_per_launch": {"candidates": wk[0], "cand_segments": wk[1],
                                              "candidate_steps_W": wk[2], "rows": wk[3], "ops": ops},
