@@ -44,6 +44,12 @@ int fail(int code, const char* msg)
 #define SDEDGE_WARPS 2
 #endif
 constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
+#ifndef SDEDGE_TILE_G
+#define SDEDGE_TILE_G 4       // DPs per warp of the tiled DP (tile = 32 / G rows)
+#endif
+#ifndef SDEDGE_TILE_MIN_K
+#define SDEDGE_TILE_MIN_K 96  // tiled DP above this K
+#endif
 // G = DPs per warp: with ALGO_ENVELOPE and small K a warp runs G independent DPs
 // (different gamma) side by side in G lane groups of 32/G lanes, so every
 // per-row instruction (stage constants, argmin, update) serves G DPs; for
@@ -101,11 +107,11 @@ template <> struct Pair<double> { using T = double2; };
 template <> struct Pair<float> { using T = float2; };
 template <typename R> using R2 = typename Pair<R>::T;
 
-// One DP row (AoS).  80 B for fp64 (40 B for fp32): with consecutive rows on
+// One DP row (AoS).  80 B for fp64 (48 B for fp32): with consecutive rows on
 // consecutive lanes the 16-byte loads of a warp hit distinct banks, and one
 // address computation serves all five loads.
 template <typename R>
-struct alignas(sizeof(R2<R>)) RowRec {
+struct alignas(16) RowRec {                  // 80 B (fp64) / 48 B (fp32): 16-byte multiples for TMA
     R2<R> Y;           // (Upsilon[p,1,0], Upsilon[p,1,1])
     R2<R> A;           // Upsilon[p,n,0] = A.x + A.y (n-1), n >= 2
     R2<R> E;           // (sum_{n=2}^{N} Upsilon[p,n,1], last m of the first envelope segment)
@@ -352,8 +358,22 @@ struct Smem {
     unsigned char* rows; // [kWarps] row states when rows_in_smem
 };
 
+#ifndef SDEDGE_TILE_CH
+#define SDEDGE_TILE_CH 8      // rows per TMA chunk of the tiled DP's phase A
+#endif
+constexpr int kTileCh = SDEDGE_TILE_CH;
+
+// per tiled DP: tile rows, their stage coefficients, two TMA staging buffers
+// (one extra row each for the 16-byte alignment of fp32 records), two mbarriers
 template <typename R, int G>
-__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
+__host__ __device__ inline size_t tile_bytes()
+{
+    return (size_t)(32 / G) * (sizeof(RowRec<R>) + sizeof(RowCoef)) +
+           2 * (size_t)(kTileCh + 1) * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
+}
+
+template <typename R, int G>
+__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile)
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
@@ -362,6 +382,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem)
     b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
     if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K);
+    if (tile) b += (size_t)kWarps * G * tile_bytes<R, G>();
     return b;
 }
 
@@ -715,12 +736,339 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     return T_last;
 }
 
+// ------------------------------------------------------------ TMA bulk copies (sm_90+/sm_100a)
+__device__ inline unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ inline void mbar_init(unsigned long long* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ inline void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// one-shot: arrive with an expected transaction count, then a 1-D bulk copy
+// global -> shared that completes the transaction on the same mbarrier
+__device__ inline void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar)
+{
+    // the buffer was last read through the generic proxy (ordered by __syncwarp)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ inline void mbar_wait(unsigned long long* bar, unsigned phase)
+{
+    unsigned done = 0;
+    for (long long spin = 0; !done; ++spin) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+        if (spin > (1LL << 28)) __trap();   // a lost transaction must fail the launch, not hang the GPU
+    }
+}
+
+// generic-proxy global stores -> visible to later async-proxy (TMA) reads
+__device__ inline void fence_proxy_async_global()
+{
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// ------------------------------------------------------------ tiled DP (large K)
+// Record-pointer versions of the segment walk, candidate and update (the
+// predecessor may live in global memory or in the shared tile buffer).
+template <typename R>
+__device__ inline Seg<R> get_seg_rec(const RowRec<R>* q, const Pool<R>& pl, int k, int c, int Mx)
+{
+    Seg<R> sg;
+    if (k == 0) {
+        sg.u = 1; sg.v = (int)q->E.y; sg.a = q->Ln.x; sg.s = q->Ln.y;
+    } else {
+        const long long o = q->off + k - 1;
+        sg.u = pl.u[o]; sg.a = pl.a[o]; sg.s = pl.s[o];
+        sg.v = (k + 1 < c) ? pl.u[o + 1] - 1 : Mx;
+    }
+    return sg;
+}
+
+template <typename R>
+__device__ __noinline__ R extra_segments_rec(const RowRec<R>* q, const Pool<R>& pl, int cntp, R P, R Q, int Mx)
+{
+    R pos = (R)0;
+    for (int k = 1; k < cntp; ++k) {
+        const Seg<R> sg = get_seg_rec(q, pl, k, cntp, Mx);
+        pos += pos_sum(P - sg.a, Q - sg.s, (R)sg.u, (R)sg.v);
+    }
+    return pos;
+}
+
+// T_{i,j} for predecessor record q (see env_cand).
+template <typename R>
+__device__ inline R env_cand_rec(const RowRec<R>* q, const Pool<R>& pl, const DPConst& D, const RowCoef& rc,
+                                 double bd, int Mx, R& rest, int& nseg)
+{
+    const R2<R> y = q->Y, a = q->A, e = q->E, ln = q->Ln;
+    const int cntp = q->cnt;
+    const R Td1 = (R)fma(bd, rc.td1, D.c2dg), Tv1 = (R)fma(bd, rc.tv1, D.c2vv);
+    const R P = a.x + (R)fma(bd, rc.ad, D.c2dg), Q = a.y + (R)(bd * D.bdc);
+    const R base = e.x + (R)fma(bd, rc.tvb, rc.tvc);
+    const R d1 = rmax(y.x + Td1, y.y) + Tv1;
+    const R dP = P - ln.x, dQ = Q - ln.y;
+    const R Du = dP + dQ, Dv = fma(dQ, e.y, dP);
+    const bool pu = Du > (R)0, pv = Dv > (R)0;
+    R pos = (pu && pv) ? (Du + Dv) * e.y * (R)0.5 : (R)0;
+    if (pu != pv && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)e.y, Du, Dv);
+    if (cntp > 1) pos += extra_segments_rec(q, pl, cntp, P, Q, Mx);
+    nseg = cntp;
+    rest = base + pos;
+    return d1 + rest;
+}
+
+// General merge of the new line into env_q (rare path, out of line so that its
+// registers do not count against the DP loop); see env_update.
+template <typename R>
+__device__ __noinline__ bool row_merge_rec(const RowRec<R>* q, RowRec<R>* o, const Pool<R>& pl, R P, R Q, R Av,
+                                           R Bv, R rest, int Mx, long long& top)
+{
+    const int cntp = q->cnt;
+    int mlo = 0, mhi = -1;
+    for (int k = 0; k < cntp && mlo == 0; ++k) {
+        const Seg<R> sg = get_seg_rec(q, pl, k, cntp, Mx);
+        const R sP = P - sg.a, sQ = Q - sg.s;
+        if (fma(sQ, (R)sg.u, sP) > (R)0 || fma(sQ, (R)sg.v, sP) > (R)0) mlo = first_pos(sP, sQ, sg.u, sg.v);
+    }
+    if (mlo > 0)
+        for (int k = cntp - 1; k >= 0; --k) {
+            const Seg<R> sg = get_seg_rec(q, pl, k, cntp, Mx);
+            const R sP = P - sg.a, sQ = Q - sg.s;
+            if (fma(sQ, (R)sg.u, sP) > (R)0 || fma(sQ, (R)sg.v, sP) > (R)0) {
+                mhi = last_pos(sP, sQ, sg.u, sg.v);
+                break;
+            }
+        }
+    const long long base = top;
+    int nseg = 0;
+    bool ovf = false;
+    R lv = (R)Mx;
+    R2<R> first{(R)0, (R)0};
+    auto emit = [&](int u, R ea, R es) {
+        ea += Av;
+        es += Bv;
+        if (nseg == 0) first = R2<R>{ea, es};
+        else {
+            if (nseg == 1) lv = (R)(u - 1);
+            const long long w = base + nseg - 1;
+            if (w >= pl.cap) ovf = true;
+            else { pl.u[w] = u; pl.a[w] = ea; pl.s[w] = es; }
+        }
+        ++nseg;
+    };
+    bool line_done = false;
+    for (int k = 0; k < cntp; ++k) {
+        const Seg<R> sg = get_seg_rec(q, pl, k, cntp, Mx);
+        if (mlo > 0 && sg.v >= mlo && sg.u <= mhi) {
+            if (sg.u < mlo) emit(sg.u, sg.a, sg.s);
+            if (!line_done) { emit(mlo, P, Q); line_done = true; }
+            if (sg.v > mhi) emit(mhi + 1, sg.a, sg.s);
+        } else {
+            emit(sg.u, sg.a, sg.s);
+        }
+    }
+    o->Ln = first;
+    o->E = R2<R>{rest, lv};
+    o->cnt = ovf ? 1 : nseg;                 // on overflow keep later reads in bounds
+    top = base + (nseg > 1 ? nseg - 1 : 0);
+    return ovf;
+}
+
+// Row i from predecessor record q and the winning candidate (eq:tt1, eq:tt2):
+// writes the full record into *o (shared tile slot); returns true on pool overflow.
+template <typename R>
+__device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o, const Pool<R>& pl, const DPConst& D,
+                               const RowCoef& rc, double bd, R rest, int Mx, long long& top)
+{
+    const R2<R> y = q->Y, a = q->A, ln = q->Ln;
+    const int cntp = q->cnt;
+    const R d0 = y.x + (R)fma(bd, rc.td1, D.c2dg);
+    const R d1 = rmax(d0, y.y) + (R)fma(bd, rc.tv1, D.c2vv);
+    const R P = a.x + (R)fma(bd, rc.ad, D.c2dg), Q = a.y + (R)(bd * D.bdc);
+    const R Av = (R)fma(bd, rc.av, D.c2vv), Bv = (R)(bd * D.bvc);
+    o->Y = R2<R>{d0, d1};
+    o->A = R2<R>{P, Q};
+    o->off = (int)top;
+    if (cntp == 0) { o->E = R2<R>{rest, (R)0}; o->Ln = R2<R>{(R)0, (R)0}; o->cnt = 0; return false; }
+    const R dP = P - ln.x, dQ = Q - ln.y;
+    const bool pu = dP + dQ > (R)0, pv = fma(dQ, (R)Mx, dP) > (R)0;
+    if (cntp == 1 && pu == pv) {             // no crossing: one line, old or new
+        o->Ln = pu ? R2<R>{P + Av, Q + Bv} : R2<R>{ln.x + Av, ln.y + Bv};
+        o->E = R2<R>{rest, (R)Mx};
+        o->cnt = 1;
+        return false;
+    }
+    return row_merge_rec(q, o, pl, P, Q, Av, Bv, rest, Mx, top);
+}
+
+// Algorithm 1 in tiles of GL rows.  Phase A: lane r of a group owns row i0+r and
+// scans every predecessor p < i0 (all final), with the whole group reading the
+// same global row record (a broadcast) -- no per-row warp work.  Phase B: the
+// in-tile triangle row by row: lanes q < r evaluate p = i0+q from the shared
+// tile buffer, lane r contributes its phase-A best, a masked REDUX picks j*,
+// and the owner writes row i0+r to the tile buffer and to the global store.
+// Same candidates, same comparisons, same tie rule as dp_gamma.
+template <typename R, int G>
+__device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, RowRec<R>* tb,
+                                 RowCoef* rcb, RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
+                                 DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
+                                 double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
+{
+    constexpr int GL = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % GL;
+    const unsigned gmask = G == 1 ? 0xffffffffu : (((1u << GL) - 1u) << (lane - gl));
+    const int K = C.K;
+    const double L = expected_tokens(alpha, gamma);
+    const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
+    const int Mx = N - 1;
+    DPConst Dl;
+    DPConst& D0 = Dl;
+    D0.g = gamma;
+    D0.tri = D0.g * (D0.g - 1.0) * 0.5;
+    D0.kd = c1d * (4.0 * C.Jd * (double)C.hd);
+    D0.kv = c1v * (4.0 * C.Jv * (double)C.hv);
+    D0.hd2 = 2.0 * C.hd + C.h2d;
+    D0.hv2 = 2.0 * C.hv + C.h2v;
+    D0.bdc = D0.kd * D0.g * L;
+    D0.bvc = D0.kv * (1.0 + D0.g) * L;
+    D0.c2dg = D0.g * c2d;
+    D0.c2vv = c2v + C.dl;
+    D0.Mx = Mx;
+    D0.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
+    // the per-(scenario, gamma) constants live in shared memory: they are read
+    // once per tile, and keeping all twelve in registers spills the phase-A loop
+    if (gl == 0) *Ds = Dl;
+    __syncwarp();
+    const DPConst& D = *Ds;
+    unsigned n_cand = 0, n_seg = 0;
+    long long top = 0;                       // pool bump pointer (kept identical in all group lanes)
+    if (gl == 0) {                           // row 0 == 0 (reading A3)
+        rw[0].Y = R2<R>{(R)0, (R)0};
+        rw[0].A = R2<R>{(R)0, (R)0};
+        rw[0].E = R2<R>{(R)0, (R)Mx};
+        rw[0].Ln = R2<R>{(R)0, (R)0};
+        rw[0].off = 0;
+        rw[0].cnt = Mx >= 1 ? 1 : 0;
+        fence_proxy_async_global();
+    }
+    __syncwarp();
+    double T_last = 0.0;
+    int rows_done = 0;
+    bool ovf_any = false, infeasible = false;
+    for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
+        const int i = i0 + gl;               // this lane's row
+        const bool own = i <= K;
+        const int jlo_i = own ? sm.jlo[i - 1] : K + 2;
+        RowCoef rc{};
+        if (own) {
+            rc = row_coef(D, sm.Is[i - 1]);
+            rcb[gl] = rc;
+        }
+        // ---- phase A: predecessors p < i0 (final rows, global store)
+        R bT = kinf<R>();
+        int bj = -1;
+        R brest = (R)0;
+        const int pA = __reduce_min_sync(0xffffffffu, jlo_i) - 1;   // jlo is gamma-independent
+        const int p0 = max(pA, 0);
+        double bd = (double)(i - p0);
+        // Predecessor rows p0 .. i0-1 stream through two shared staging buffers by
+        // TMA bulk copies (cp.async.bulk + mbarrier): chunk c+1 is in flight while
+        // chunk c is consumed with broadcast shared loads.
+        static_assert(sizeof(RowRec<R>) % 16 == 0, "TMA bulk copies need 16-byte multiples");
+        constexpr int ALN = 1;
+        const int nrows = i0 - p0;
+        const int nch = (nrows + kTileCh - 1) / kTileCh;
+        if (gl == 0 && nch > 0) {
+            const int e = min(p0 + kTileCh, i0), a16 = p0 - p0 % ALN;   // 16-byte aligned global start
+            bulk_load(stage, rw + a16, (unsigned)((e - a16) * sizeof(RowRec<R>)), bars);
+        }
+        for (int c = 0; c < nch; ++c) {
+            if (gl == 0 && c + 1 < nch) {
+                const int a1 = p0 + (c + 1) * kTileCh, e1 = min(a1 + kTileCh, i0), a16 = a1 - a1 % ALN;
+                bulk_load(stage + ((c + 1) & 1) * (kTileCh + 1), rw + a16,
+                          (unsigned)((e1 - a16) * sizeof(RowRec<R>)), bars + ((c + 1) & 1));
+            }
+            mbar_wait(bars + (c & 1), (bar_phase >> (c & 1)) & 1u);
+            bar_phase ^= 1u << (c & 1);
+            const int a = p0 + c * kTileCh, e = min(a + kTileCh, i0);
+            const RowRec<R>* buf = stage + (c & 1) * (kTileCh + 1) + (a % ALN);
+            for (int p = a; p < e; ++p, bd -= 1.0) {
+                R r0;
+                int c0;
+                const R T0 = env_cand_rec(buf + (p - a), pl, D, rc, bd, Mx, r0, c0);
+                if (own && p + 1 >= jlo_i) {
+                    n_cand += 1;
+                    n_seg += (unsigned)c0;
+                    if (T0 <= bT) { bT = T0; bj = p + 1; brest = r0; }   // ascending j: '<=' keeps the largest
+                }
+            }
+            __syncwarp();                                        // buffer (c & 1) may be refilled now
+        }
+        __syncwarp();
+        // ---- phase B: the in-tile triangle, row by row
+        for (int r = 0; r < GL; ++r) {
+            const int ii = i0 + r;
+            if (ii > K) break;
+            const int jlo = sm.jlo[ii - 1];
+            if (jlo > ii) { infeasible = true; break; }
+            const RowCoef rr = rcb[r];
+            R t = kinf<R>(), rq = (R)0;
+            int jq = -1;
+            if (gl < r && i0 + gl + 1 >= jlo) {   // candidate j = i0+gl+1, predecessor p = i0+gl (in tile)
+                int c0;
+                t = env_cand_rec(tb + gl, pl, D, rr, (double)(ii - (i0 + gl)), Mx, rq, c0);
+                jq = i0 + gl + 1;
+                n_cand += 1;
+                n_seg += (unsigned)c0;
+            }
+            if (gl == r) { t = bT; jq = bj; rq = brest; }   // the phase-A best of row ii
+            R tmin;
+            const int jj = warp_argmin(t, jq, &tmin, gmask);
+            if (jj < 0) { infeasible = true; break; }
+            if (jq == jj && (gl == r ? true : gl < r)) {   // the owner (one lane per group)
+                if (S) S[ii - 1] = (short)jj;
+                const int p = jj - 1;
+                const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
+                if (row_update_rec(q, tb + r, pl, D, rr, (double)(ii - p), rq, Mx, top)) ovf_any = true;
+                rw[ii] = tb[r];
+                fence_proxy_async_global();      // later tiles read this row through TMA
+            }
+            // every group lane follows the owner's pool pointer
+            const unsigned own_mask = __ballot_sync(0xffffffffu, jq == jj && (gl == r || gl < r)) & gmask;
+            top = __shfl_sync(0xffffffffu, top, __ffs(own_mask) - 1);
+            __syncwarp();
+            ++rows_done;
+            T_last = (double)tmin;
+        }
+    }
+    if (infeasible) T_last = dinf();
+    if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
+    if (active) {
+        wc.cand += n_cand;
+        wc.seg += n_seg;
+        wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
+        if (gl == 0) wc.rows += rows_done;
+    }
+    return T_last;
+}
+
 // ------------------------------------------------------------ the fused kernel
 #ifndef SDEDGE_MINB
 #define SDEDGE_MINB 8     // min resident CTAs per SM requested from ptxas (128-register cap)
 #endif
 
-template <typename R, int ALGO, int RSMEM, int G>
+template <typename R, int ALGO, int RSMEM, int G, int TILE>
 __global__ void __launch_bounds__(kThreads, SDEDGE_MINB)
 solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws, int BIG)
 {
@@ -737,6 +1085,27 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)(warp * G + grp) * rows_bytes<R>(K)
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
+    RowRec<R>* tb = nullptr;
+    RowCoef* rcb = nullptr;
+    RowRec<R>* stage = nullptr;
+    unsigned long long* bars = nullptr;
+    DPConst* dpc = nullptr;
+    if (TILE) {                              // shared tile buffer of this (warp, group) DP
+        unsigned char* t = sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K) : 0) +
+                           (size_t)(warp * G + grp) * tile_bytes<R, G>();
+        tb = reinterpret_cast<RowRec<R>*>(t);
+        rcb = reinterpret_cast<RowCoef*>(t + (size_t)GL * sizeof(RowRec<R>));
+        stage = reinterpret_cast<RowRec<R>*>(t + (size_t)GL * (sizeof(RowRec<R>) + sizeof(RowCoef)));
+        bars = reinterpret_cast<unsigned long long*>(stage + 2 * (kTileCh + 1));
+        dpc = reinterpret_cast<DPConst*>(bars + 2);
+        if (lane % GL == 0) {
+            mbar_init(bars, 1);
+            mbar_init(bars + 1, 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+    }
+    unsigned bar_phase = 0u;                  // parity of each staging mbarrier (bit b)
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     __shared__ bool s_ovf;
     __shared__ unsigned long long s_work[4];
@@ -850,8 +1219,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 short* Sg = active ? sm.S + (size_t)gi * K : nullptr;
                 const short* jf = (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX)
                                       ? sm.jf : nullptr;
-                double t;
-                if (C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
+                double t = 0.0;
+                // baselines run only in the G = 1, untiled instantiations (launch_all), so the
+                // other instantiations compile just their own DP (fewer live registers)
+                constexpr bool kBase = G == 1 && !TILE;
+                if constexpr (TILE) {
+                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, rcb, stage, bars, bar_phase, dpc, C.gmin + gi, alpha,
+                                             c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active);
+                } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
                     // 2, 3, ... in sorted order until the pipelined latency stops improving
                     short* jw = sm.jw + (size_t)warp * K;
@@ -880,7 +1255,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                                              &s_top[warp * G + grp], active, jw);
                 } else {
                     t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v, Sg, &ovf, wc,
-                                             &s_top[warp * G + grp], active, jf);
+                                             &s_top[warp * G + grp], active, kBase ? jf : nullptr);
                 }
                 if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
@@ -1120,7 +1495,7 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
         }                                                                       \
     } while (0)
 
-template <typename R, int ALGO, int G>
+template <typename R, int ALGO, int G, int TILE>
 int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long n, cudaStream_t st, int flags)
 {
     int dev = 0, nsm = 0, max_smem = 0;
@@ -1131,16 +1506,12 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     Consts C = C0;
     const size_t rb = rows_bytes<R>(C.K);
     // row state in shared memory when it keeps >= 3 CTAs (12 warps) per SM
-#ifdef SDEDGE_ROWS_GLOBAL
-    C.rows_in_smem = 0;
-#else
-    C.rows_in_smem = smem_bytes<R, G>(C.K, C.ng, 1) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
-#endif
-    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem);
+    C.rows_in_smem = !TILE && smem_bytes<R, G>(C.K, C.ng, 1, 0) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
+    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE);
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
-    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1, G> : solve_kernel<R, ALGO, 0, G>;
+    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1, G, TILE> : solve_kernel<R, ALGO, 0, G, TILE>;
     auto k_big = k_main;
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
@@ -1221,20 +1592,25 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
                 reinterpret_cast<unsigned long long*>(o->work_counters)};
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
-    // DPs per warp (envelope): 4 for small K, 2 for medium, 1 for large (r01 sweep)
-    const int G = (p->algo == SDEDGE_ALGO_DENSE || p->batching_policy != SDEDGE_BATCH_PROPOSED)
-                      ? 1 : (p->K <= 48 ? 4 : p->K <= 96 ? 2 : 1);
+    // envelope, proposed policy: small K -> G DPs per warp with row state in shared
+    // memory; larger K -> the tiled DP (rows in global memory, a GL-row shared tile
+    // per DP) with SDEDGE_TILE_G DPs per warp.  Baselines and dense: one DP per warp.
     const int f = p->flags;
+    const bool base = p->algo == SDEDGE_ALGO_DENSE || p->batching_policy != SDEDGE_BATCH_PROPOSED;
+    const bool tiled = !base && p->K > SDEDGE_TILE_MIN_K;
+    const int G = base ? 1 : (p->K <= 48 ? 4 : 2);
     if (p->precision == 0) {
-        if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<double, SDEDGE_ALGO_DENSE, 1>(C, in, out, n, st, f);
-        if (G == 4) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 4>(C, in, out, n, st, f);
-        if (G == 2) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 2>(C, in, out, n, st, f);
-        return launch_all<double, SDEDGE_ALGO_ENVELOPE, 1>(C, in, out, n, st, f);
+        if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<double, SDEDGE_ALGO_DENSE, 1, 0>(C, in, out, n, st, f);
+        if (base) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 1, 0>(C, in, out, n, st, f);
+        if (tiled) return launch_all<double, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 1>(C, in, out, n, st, f);
+        if (G == 4) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 4, 0>(C, in, out, n, st, f);
+        return launch_all<double, SDEDGE_ALGO_ENVELOPE, 2, 0>(C, in, out, n, st, f);
     }
-    if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<float, SDEDGE_ALGO_DENSE, 1>(C, in, out, n, st, f);
-    if (G == 4) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 4>(C, in, out, n, st, f);
-    if (G == 2) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 2>(C, in, out, n, st, f);
-    return launch_all<float, SDEDGE_ALGO_ENVELOPE, 1>(C, in, out, n, st, f);
+    if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<float, SDEDGE_ALGO_DENSE, 1, 0>(C, in, out, n, st, f);
+    if (base) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 1, 0>(C, in, out, n, st, f);
+    if (tiled) return launch_all<float, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 1>(C, in, out, n, st, f);
+    if (G == 4) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 4, 0>(C, in, out, n, st, f);
+    return launch_all<float, SDEDGE_ALGO_ENVELOPE, 2, 0>(C, in, out, n, st, f);
 }
 
 }  // namespace

@@ -319,3 +319,31 @@ def test_actual_output_evaluation(cfg, pair, n, pol):
                               torch.full((n, K), pd["O_max"], dtype=torch.int32, device=dev), plan, co)
     torch.cuda.synchronize()
     assert np.allclose(full.cpu().numpy(), pl["lat"][:, 2], rtol=1e-12, atol=0)
+
+
+def test_c4_fp32_tiled():
+    """fp32 variant through the tiled large-K DP (TMA-staged predecessor rows)."""
+    pd, sc, _ = scengen.config("C4", 0, 400)
+    orc_idx = np.arange(0, 400, 50)
+    sub = {k: (v[orc_idx] if v is not None else None) for k, v in sc.items()}
+    orc = oracle.solve_batch(pd, sub)
+    g = gpu_solve(pd, sc, precision=1)
+    res = compare(pd, sc, g, orc, 1, oracle, idx=orc_idx)
+    assert res["failures"] == 0
+    g64 = gpu_solve(pd, sc, precision=0)
+    assert np.allclose(g["lat"], g64["lat"], rtol=1e-5, atol=0)
+
+
+def test_overflow_second_pass_tiled():
+    """The tiny first-pass pool at K = 128 (tiled DP) with the slow 1.1B draft
+    (multi-segment envelopes): identical results through the worst-case pass."""
+    pd = scengen.params("1.1B-7B", K=128, gamma_min=1, gamma_max=8, c1_draft=4 * 4.11e-13)
+    _, sc, _ = scengen.config("C4", 0, 300)
+    a = gpu_solve(pd, sc)
+    b = gpu_solve(dict(pd, flags=1), sc)
+    for k in a:
+        if a[k] is not None:
+            assert np.array_equal(a[k], b[k]), k
+    idx = np.arange(0, 300, 60)
+    sub = {k: (v[idx] if v is not None else None) for k, v in sc.items()}
+    compare(pd, sc, a, oracle.solve_batch(pd, sub), 0, oracle, idx=idx)
