@@ -47,6 +47,9 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_G
 #define SDEDGE_TILE_G 4       // DPs per warp of the tiled DP (tile = 32 / G rows)
 #endif
+#ifndef SDEDGE_TILE_SHFL_ARGMIN
+#define SDEDGE_TILE_SHFL_ARGMIN 1
+#endif
 #ifndef SDEDGE_TILE_MIN_K
 #define SDEDGE_TILE_MIN_K 96  // tiled DP above this K
 #endif
@@ -184,6 +187,36 @@ __device__ inline int warp_argmin(float t, int j, float* tmin, unsigned mask)
     const unsigned m = __reduce_min_sync(mask, key);
     *tmin = __uint_as_float(m);
     return __reduce_max_sync(mask, key == m ? j : -1);
+}
+
+// Argmin within an aligned group of GL lanes by a butterfly of shuffles on the
+// (T bits, j) key -- same order and tie rule as warp_argmin.
+template <int GL>
+__device__ inline int group_argmin(double t, int j, double* tmin)
+{
+    unsigned long long key = (unsigned long long)__double_as_longlong(t);
+#pragma unroll
+    for (int o = GL / 2; o > 0; o >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+        if (ok < key || (ok == key && oj > j)) { key = ok; j = oj; }
+    }
+    *tmin = __longlong_as_double((long long)key);
+    return j;
+}
+
+template <int GL>
+__device__ inline int group_argmin(float t, int j, float* tmin)
+{
+    unsigned key = __float_as_uint(t);
+#pragma unroll
+    for (int o = GL / 2; o > 0; o >>= 1) {
+        const unsigned ok = __shfl_xor_sync(0xffffffffu, key, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+        if (ok < key || (ok == key && oj > j)) { key = ok; j = oj; }
+    }
+    *tmin = __uint_as_float(key);
+    return j;
 }
 
 // First / last integer m in [u, v] with dP + dQ m > 0, given that the sign
@@ -1034,7 +1067,11 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             }
             if (gl == r) { t = bT; jq = bj; rq = brest; }   // the phase-A best of row ii
             R tmin;
+#if SDEDGE_TILE_SHFL_ARGMIN
+            const int jj = group_argmin<GL>(t, jq, &tmin);
+#else
             const int jj = warp_argmin(t, jq, &tmin, gmask);
+#endif
             if (jj < 0) { infeasible = true; break; }
             if (jq == jj && (gl == r ? true : gl < r)) {   // the owner (one lane per group)
                 if (S) S[ii - 1] = (short)jj;
