@@ -721,7 +721,11 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
             }
         }
         R tmin;
+#if SDEDGE_TILE_SHFL_ARGMIN
+        const int jj = G > 1 ? group_argmin<GL>(bT, bj, &tmin) : warp_argmin(bT, bj, &tmin, gmask);
+#else
         const int jj = warp_argmin(bT, bj, &tmin, gmask);
+#endif
         // Every lane prepares row i as if its own best candidate won (SIMD, so this
         // overlaps the REDUX latency instead of serialising behind it); the owner of
         // j* then only stores.  eq:rg, eq:tt1, eq:tt2 (reading A4: S[i] always set).
