@@ -48,10 +48,11 @@ OPS = {"dense": dict(cand=16, seg=0, step=4, row=40),
        "envelope": dict(cand=16, seg=10, step=0, row=40)}
 
 # DRAM bytes (read + write) per scenario of the envelope kernel from the one
-# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_c4.md: 268.3 MB
-# read + 182.1 MB written for a 1e5-scenario C4 launch), scaled to the launch.
-# The algorithmic bytes are 2568 in + 2084 out per scenario.
-NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (268.348928e6 + 182.146304e6) / 1e5}
+# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_tiled_c4.md:
+# 2.06 GB read + 14.69 GB written for a 1e5-scenario C4 launch), scaled to the
+# launch.  The algorithmic bytes are 2568 in + 2084 out per scenario; the rest
+# is the write-back of the tiled DP's global row store.
+NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (2.060626e9 + 14.687073e9) / 1e5}
 
 
 def parse():

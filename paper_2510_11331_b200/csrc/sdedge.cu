@@ -842,6 +842,17 @@ __device__ __noinline__ R extra_segments_rec(const RowRec<R>* q, const Pool<R>& 
     return pos;
 }
 
+// The rare parts of a candidate's envelope sum, behind one branch: a crossing
+// inside the first segment and/or further segments.
+template <typename R>
+__device__ __noinline__ R rare_pos(const RowRec<R>* q, const Pool<R>& pl, int cntp, R P, R Q, R dP, R dQ, R Du,
+                                   R Dv, bool cross, R pos, int Mx)
+{
+    if (cross && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)q->E.y, Du, Dv);
+    if (cntp > 1) pos += extra_segments_rec(q, pl, cntp, P, Q, Mx);
+    return pos;
+}
+
 // T_{i,j} for predecessor record q (see env_cand).
 template <typename R>
 __device__ inline R env_cand_rec(const RowRec<R>* q, const Pool<R>& pl, const DPConst& D, const RowCoef& rc,
@@ -857,8 +868,7 @@ __device__ inline R env_cand_rec(const RowRec<R>* q, const Pool<R>& pl, const DP
     const R Du = dP + dQ, Dv = fma(dQ, e.y, dP);
     const bool pu = Du > (R)0, pv = Dv > (R)0;
     R pos = (pu && pv) ? (Du + Dv) * e.y * (R)0.5 : (R)0;
-    if (pu != pv && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)e.y, Du, Dv);
-    if (cntp > 1) pos += extra_segments_rec(q, pl, cntp, P, Q, Mx);
+    if ((pu != pv) | (cntp > 1)) pos = rare_pos(q, pl, cntp, P, Q, dP, dQ, Du, Dv, pu != pv, pos, Mx);
     nseg = cntp;
     rest = base + pos;
     return d1 + rest;
