@@ -831,13 +831,15 @@ __device__ inline Seg<R> get_seg_rec(const RowRec<R>* q, const Pool<R>& pl, int 
     return sg;
 }
 
+// Segments k >= 1 of an envelope whose extra segments start at pool[off].
 template <typename R>
-__device__ __noinline__ R extra_segments_rec(const RowRec<R>* q, const Pool<R>& pl, int cntp, R P, R Q, int Mx)
+__device__ __noinline__ R extra_segments_off(const Pool<R>& pl, int off, int cntp, R P, R Q, int Mx)
 {
     R pos = (R)0;
     for (int k = 1; k < cntp; ++k) {
-        const Seg<R> sg = get_seg_rec(q, pl, k, cntp, Mx);
-        pos += pos_sum(P - sg.a, Q - sg.s, (R)sg.u, (R)sg.v);
+        const long long o = off + k - 1;
+        const int u = pl.u[o], v = (k + 1 < cntp) ? pl.u[o + 1] - 1 : Mx;
+        pos += pos_sum(P - pl.a[o], Q - pl.s[o], (R)u, (R)v);
     }
     return pos;
 }
@@ -845,11 +847,11 @@ __device__ __noinline__ R extra_segments_rec(const RowRec<R>* q, const Pool<R>& 
 // The rare parts of a candidate's envelope sum, behind one branch: a crossing
 // inside the first segment and/or further segments.
 template <typename R>
-__device__ __noinline__ R rare_pos(const RowRec<R>* q, const Pool<R>& pl, int cntp, R P, R Q, R dP, R dQ, R Du,
+__device__ __noinline__ R rare_pos(const Pool<R>& pl, int cntp, int off, R lv, R P, R Q, R dP, R dQ, R Du,
                                    R Dv, bool cross, R pos, int Mx)
 {
-    if (cross && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)q->E.y, Du, Dv);
-    if (cntp > 1) pos += extra_segments_rec(q, pl, cntp, P, Q, Mx);
+    if (cross && cntp > 0) pos = crossing_sum(dP, dQ, 1, (int)lv, Du, Dv);
+    if (cntp > 1) pos += extra_segments_off(pl, off, cntp, P, Q, Mx);
     return pos;
 }
 
@@ -859,7 +861,7 @@ __device__ inline R env_cand_rec(const RowRec<R>* q, const Pool<R>& pl, const DP
                                  double bd, int Mx, R& rest, int& nseg)
 {
     const R2<R> y = q->Y, a = q->A, e = q->E, ln = q->Ln;
-    const int cntp = q->cnt;
+    const int cntp = q->cnt, off = q->off;
     const R Td1 = (R)fma(bd, rc.td1, D.c2dg), Tv1 = (R)fma(bd, rc.tv1, D.c2vv);
     const R P = a.x + (R)fma(bd, rc.ad, D.c2dg), Q = a.y + (R)(bd * D.bdc);
     const R base = e.x + (R)fma(bd, rc.tvb, rc.tvc);
@@ -868,7 +870,7 @@ __device__ inline R env_cand_rec(const RowRec<R>* q, const Pool<R>& pl, const DP
     const R Du = dP + dQ, Dv = fma(dQ, e.y, dP);
     const bool pu = Du > (R)0, pv = Dv > (R)0;
     R pos = (pu && pv) ? (Du + Dv) * e.y * (R)0.5 : (R)0;
-    if ((pu != pv) | (cntp > 1)) pos = rare_pos(q, pl, cntp, P, Q, dP, dQ, Du, Dv, pu != pv, pos, Mx);
+    if ((pu != pv) | (cntp > 1)) pos = rare_pos(pl, cntp, off, e.y, P, Q, dP, dQ, Du, Dv, pu != pv, pos, Mx);
     nseg = cntp;
     rest = base + pos;
     return d1 + rest;
@@ -1093,7 +1095,6 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                 const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
                 if (row_update_rec(q, tb + r, pl, D, rr, (double)(ii - p), rq, Mx, top)) ovf_any = true;
                 rw[ii] = tb[r];
-                fence_proxy_async_global();      // later tiles read this row through TMA
             }
             // every group lane follows the owner's pool pointer
             const unsigned own_mask = __ballot_sync(0xffffffffu, jq == jj && (gl == r || gl < r)) & gmask;
@@ -1102,6 +1103,10 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             ++rows_done;
             T_last = (double)tmin;
         }
+        // later tiles bulk-read this tile's rows through TMA (async proxy): every
+        // lane orders the global row stores it made before the next __syncwarp
+        fence_proxy_async_global();
+        __syncwarp();
     }
     if (infeasible) T_last = dinf();
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
@@ -1546,11 +1551,26 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
         }                                                                       \
     } while (0)
 
+// Keep stream-ordered workspace cached in the device's default pool between
+// calls (the default release threshold of 0 returns it at every sync point).
+int keep_pool_cached(int dev)
+{
+    static thread_local int done_mask = 0;   // devices < 32 handled on this thread
+    if (dev < 32 && (done_mask >> dev & 1)) return 0;
+    cudaMemPool_t pool;
+    CU(cudaDeviceGetDefaultMemPool(&pool, dev));
+    unsigned long long thr = ~0ULL;
+    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    if (dev < 32) done_mask |= 1 << dev;
+    return 0;
+}
+
 template <typename R, int ALGO, int G, int TILE>
 int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long n, cudaStream_t st, int flags)
 {
     int dev = 0, nsm = 0, max_smem = 0;
     CU(cudaGetDevice(&dev));
+    if (int rc = keep_pool_cached(dev)) return rc;
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
 
@@ -1688,7 +1708,7 @@ int sdedge_solve_batch(const sdedge_scenarios* s, int64_t n, const sdedge_params
 int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
                             sdedge_schedule* o)
 {
-    // Host buffers in, host buffers out.  The batch is cut into chunks that
+    // Host buffers in, host buffers out.  The batch is cut into <= 16 chunks that
     // alternate between two internal streams, so the H2D copy of chunk c+1 and
     // the D2H copy of chunk c-1 overlap the solve of chunk c; the caller's
     // stream is joined at the end (one cudaMemcpyAsync per array and chunk).
@@ -1707,6 +1727,9 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     const size_t oLat = take(bLat), oGm = take(bS), oM = take(bS), oBe = take(bI), oOr = take(bI),
                  oW = take(bW), oSt = take(bS);
     unsigned char* d = nullptr;
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    if (int rc2 = keep_pool_cached(dev)) return rc2;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&d), off, st));
     cudaStream_t ss[2] = {nullptr, nullptr};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -1715,7 +1738,7 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     CU(cudaEventRecord(ev[0], st));
     for (int q = 0; q < 2; ++q) CU(cudaStreamWaitEvent(ss[q], ev[0], 0));
 
-    const long long nch = std::max(1LL, std::min(8LL, (long long)(n / 65536)));
+    const long long nch = std::max(1LL, std::min(16LL, (long long)(n / 32768)));
     const long long chunk = (n + nch - 1) / nch;
     int launches = 0;
     auto h2d = [&](size_t doff, const void* src, size_t row, long long a, long long m, cudaStream_t q) {
