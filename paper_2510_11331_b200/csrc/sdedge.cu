@@ -933,11 +933,13 @@ __device__ __noinline__ bool row_merge_rec(const RowRec<R>* q, RowRec<R>* o, con
     return ovf;
 }
 
-// Row i from predecessor record q and the winning candidate (eq:tt1, eq:tt2):
-// writes the full record into *o (shared tile slot); returns true on pool overflow.
+// Row i from predecessor record q and the winning candidate (eq:tt1, eq:tt2),
+// stored to the shared tile slot o_s and the global row store o_g; the pool
+// pointer lives in shared memory (only the rare merge path moves it).
+// Returns true on pool overflow.
 template <typename R>
-__device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o, const Pool<R>& pl, const DPConst& D,
-                               const RowCoef& rc, double bd, R rest, int Mx, long long& top)
+__device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g, const Pool<R>& pl,
+                               const DPConst& D, const RowCoef& rc, double bd, R rest, int Mx, long long* top_s)
 {
     const R2<R> y = q->Y, a = q->A, ln = q->Ln;
     const int cntp = q->cnt;
@@ -945,19 +947,25 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o, const Pool<R>& 
     const R d1 = rmax(d0, y.y) + (R)fma(bd, rc.tv1, D.c2vv);
     const R P = a.x + (R)fma(bd, rc.ad, D.c2dg), Q = a.y + (R)(bd * D.bdc);
     const R Av = (R)fma(bd, rc.av, D.c2vv), Bv = (R)(bd * D.bvc);
-    o->Y = R2<R>{d0, d1};
-    o->A = R2<R>{P, Q};
-    o->off = (int)top;
-    if (cntp == 0) { o->E = R2<R>{rest, (R)0}; o->Ln = R2<R>{(R)0, (R)0}; o->cnt = 0; return false; }
+    const R2<R> Y{d0, d1}, A{P, Q};
     const R dP = P - ln.x, dQ = Q - ln.y;
     const bool pu = dP + dQ > (R)0, pv = fma(dQ, (R)Mx, dP) > (R)0;
-    if (cntp == 1 && pu == pv) {             // no crossing: one line, old or new
-        o->Ln = pu ? R2<R>{P + Av, Q + Bv} : R2<R>{ln.x + Av, ln.y + Bv};
-        o->E = R2<R>{rest, (R)Mx};
-        o->cnt = 1;
+    if (cntp == 0 || (cntp == 1 && pu == pv)) {   // N = 1, or no crossing: one line, old or new
+        const R2<R> Ln = cntp == 0 ? R2<R>{(R)0, (R)0}
+                                   : (pu ? R2<R>{P + Av, Q + Bv} : R2<R>{ln.x + Av, ln.y + Bv});
+        const R2<R> E{rest, cntp == 0 ? (R)0 : (R)Mx};
+        o_s->Y = Y; o_s->A = A; o_s->E = E; o_s->Ln = Ln; o_s->cnt = cntp; o_s->off = 0;
+        o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0;
         return false;
     }
-    return row_merge_rec(q, o, pl, P, Q, Av, Bv, rest, Mx, top);
+    long long top = *top_s;
+    o_s->Y = Y;
+    o_s->A = A;
+    o_s->off = (int)top;
+    const bool ovf = row_merge_rec(q, o_s, pl, P, Q, Av, Bv, rest, Mx, top);
+    *top_s = top;
+    *o_g = *o_s;
+    return ovf;
 }
 
 // Algorithm 1 in tiles of GL rows.  Phase A: lane r of a group owns row i0+r and
@@ -1001,8 +1009,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     __syncwarp();
     const DPConst& D = *Ds;
     unsigned n_cand = 0, n_seg = 0;
-    long long top = 0;                       // pool bump pointer (kept identical in all group lanes)
-    if (gl == 0) {                           // row 0 == 0 (reading A3)
+    if (gl == 0) {                           // row 0 == 0 (reading A3); empty segment pool
+        *top_s = 0;
         rw[0].Y = R2<R>{(R)0, (R)0};
         rw[0].A = R2<R>{(R)0, (R)0};
         rw[0].E = R2<R>{(R)0, (R)Mx};
@@ -1093,12 +1101,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                 if (S) S[ii - 1] = (short)jj;
                 const int p = jj - 1;
                 const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
-                if (row_update_rec(q, tb + r, pl, D, rr, (double)(ii - p), rq, Mx, top)) ovf_any = true;
-                rw[ii] = tb[r];
+                if (row_update_rec(q, tb + r, rw + ii, pl, D, rr, (double)(ii - p), rq, Mx, top_s)) ovf_any = true;
             }
-            // every group lane follows the owner's pool pointer
-            const unsigned own_mask = __ballot_sync(0xffffffffu, jq == jj && (gl == r || gl < r)) & gmask;
-            top = __shfl_sync(0xffffffffu, top, __ffs(own_mask) - 1);
             __syncwarp();
             ++rows_done;
             T_last = (double)tmin;
