@@ -396,12 +396,11 @@ struct Smem {
 #endif
 constexpr int kTileCh = SDEDGE_TILE_CH;
 
-// per tiled DP: tile rows, their stage coefficients, two TMA staging buffers
-// (one extra row each for the 16-byte alignment of fp32 records), two mbarriers
+// per tiled DP: tile rows, two TMA staging buffers, two mbarriers, the DP constants
 template <typename R, int G>
 __host__ __device__ inline size_t tile_bytes()
 {
-    return (size_t)(32 / G) * (sizeof(RowRec<R>) + sizeof(RowCoef)) +
+    return (size_t)(32 / G) * sizeof(RowRec<R>) +
            2 * (size_t)(kTileCh + 1) * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
 }
 
@@ -968,16 +967,18 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_
     return ovf;
 }
 
-// Algorithm 1 in tiles of GL rows.  Phase A: lane r of a group owns row i0+r and
-// scans every predecessor p < i0 (all final), with the whole group reading the
-// same global row record (a broadcast) -- no per-row warp work.  Phase B: the
-// in-tile triangle row by row: lanes q < r evaluate p = i0+q from the shared
-// tile buffer, lane r contributes its phase-A best, a masked REDUX picks j*,
-// and the owner writes row i0+r to the tile buffer and to the global store.
-// Same candidates, same comparisons, same tie rule as dp_gamma.
+// Algorithm 1 in tiles of GL rows; lane r of a group owns row i0+r throughout.
+// Phase A: every lane scans the finished predecessors p < i0, the whole group
+// reading the same record (a broadcast from the TMA-staged chunk) -- no per-row
+// warp work.  Phase B: rows in order; lane r finalizes row i0+r from its own
+// running best (no reduction), writes it to the shared tile and the global
+// store, and the later rows of the tile evaluate their candidate with that row
+// as predecessor.  Every lane sees its row's candidates in ascending j, so the
+// '<=' update keeps the largest j: the same candidates, comparisons and tie
+// rule as dp_gamma.
 template <typename R, int G>
 __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, RowRec<R>* tb,
-                                 RowCoef* rcb, RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
+                                 RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
                                  DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
                                  double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
 {
@@ -1020,18 +1021,15 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         fence_proxy_async_global();
     }
     __syncwarp();
-    double T_last = 0.0;
     int rows_done = 0;
     bool ovf_any = false, infeasible = false;
+    R t_row = (R)0;                          // Upsilon[i,0,0] of the last row this lane finalized
     for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
         const int i = i0 + gl;               // this lane's row
         const bool own = i <= K;
         const int jlo_i = own ? sm.jlo[i - 1] : K + 2;
         RowCoef rc{};
-        if (own) {
-            rc = row_coef(D, sm.Is[i - 1]);
-            rcb[gl] = rc;
-        }
+        if (own) rc = row_coef(D, sm.Is[i - 1]);
         // ---- phase A: predecessors p < i0 (final rows, global store)
         R bT = kinf<R>();
         int bj = -1;
@@ -1073,45 +1071,41 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             __syncwarp();                                        // buffer (c & 1) may be refilled now
         }
         __syncwarp();
-        // ---- phase B: the in-tile triangle, row by row
+        // ---- phase B: the tile's rows in order.  Lane r already holds the best
+        // of every candidate of its row except those whose predecessor is in the
+        // tile; each finished row i0+r is "pushed": the later rows of the tile
+        // evaluate their candidate with predecessor i0+r (broadcast from the shared
+        // tile).  So no reduction is needed: lane r finalizes row i0+r itself.
         for (int r = 0; r < GL; ++r) {
             const int ii = i0 + r;
             if (ii > K) break;
-            const int jlo = sm.jlo[ii - 1];
-            if (jlo > ii) { infeasible = true; break; }
-            const RowCoef rr = rcb[r];
-            R t = kinf<R>(), rq = (R)0;
-            int jq = -1;
-            if (gl < r && i0 + gl + 1 >= jlo) {   // candidate j = i0+gl+1, predecessor p = i0+gl (in tile)
-                int c0;
-                t = env_cand_rec(tb + gl, pl, D, rr, (double)(ii - (i0 + gl)), Mx, rq, c0);
-                jq = i0 + gl + 1;
-                n_cand += 1;
-                n_seg += (unsigned)c0;
-            }
-            if (gl == r) { t = bT; jq = bj; rq = brest; }   // the phase-A best of row ii
-            R tmin;
-#if SDEDGE_TILE_SHFL_ARGMIN
-            const int jj = group_argmin<GL>(t, jq, &tmin);
-#else
-            const int jj = warp_argmin(t, jq, &tmin, gmask);
-#endif
-            if (jj < 0) { infeasible = true; break; }
-            if (jq == jj && (gl == r ? true : gl < r)) {   // the owner (one lane per group)
-                if (S) S[ii - 1] = (short)jj;
-                const int p = jj - 1;
+            if (sm.jlo[ii - 1] > ii) { infeasible = true; break; }   // empty window (uniform)
+            if (gl == r) {                   // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
+                if (S) S[ii - 1] = (short)bj;
+                const int p = bj - 1;
                 const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
-                if (row_update_rec(q, tb + r, rw + ii, pl, D, rr, (double)(ii - p), rq, Mx, top_s)) ovf_any = true;
+                if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s))
+                    ovf_any = true;
+                t_row = bT;
             }
             __syncwarp();
+            if (own && gl > r && ii + 1 >= jlo_i) {   // candidate j = ii+1 of the later rows
+                R rq;
+                int c0;
+                const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
+                n_cand += 1;
+                n_seg += (unsigned)c0;
+                if (t <= bT) { bT = t; bj = ii + 1; brest = rq; }   // ascending j: '<=' keeps the largest
+            }
             ++rows_done;
-            T_last = (double)tmin;
         }
         // later tiles bulk-read this tile's rows through TMA (async proxy): every
         // lane orders the global row stores it made before the next __syncwarp
         fence_proxy_async_global();
         __syncwarp();
     }
+    // T_inf = Upsilon[K,0,0], held by the lane that finalized row K
+    double T_last = (double)__shfl_sync(0xffffffffu, t_row, (lane - gl) + (K - 1) % GL);
     if (infeasible) T_last = dinf();
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
     if (active) {
@@ -1146,7 +1140,6 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     RowRec<R>* tb = nullptr;
-    RowCoef* rcb = nullptr;
     RowRec<R>* stage = nullptr;
     unsigned long long* bars = nullptr;
     DPConst* dpc = nullptr;
@@ -1154,8 +1147,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         unsigned char* t = sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K) : 0) +
                            (size_t)(warp * G + grp) * tile_bytes<R, G>();
         tb = reinterpret_cast<RowRec<R>*>(t);
-        rcb = reinterpret_cast<RowCoef*>(t + (size_t)GL * sizeof(RowRec<R>));
-        stage = reinterpret_cast<RowRec<R>*>(t + (size_t)GL * (sizeof(RowRec<R>) + sizeof(RowCoef)));
+        stage = reinterpret_cast<RowRec<R>*>(t + (size_t)GL * sizeof(RowRec<R>));
         bars = reinterpret_cast<unsigned long long*>(stage + 2 * (kTileCh + 1));
         dpc = reinterpret_cast<DPConst*>(bars + 2);
         if (lane % GL == 0) {
@@ -1284,7 +1276,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 // other instantiations compile just their own DP (fewer live registers)
                 constexpr bool kBase = G == 1 && !TILE;
                 if constexpr (TILE) {
-                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, rcb, stage, bars, bar_phase, dpc, C.gmin + gi, alpha,
+                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, dpc, C.gmin + gi, alpha,
                                              c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
