@@ -51,7 +51,7 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #define SDEDGE_TILE_SHFL_ARGMIN 1
 #endif
 #ifndef SDEDGE_TILE_MIN_K
-#define SDEDGE_TILE_MIN_K 96  // tiled DP above this K
+#define SDEDGE_TILE_MIN_K 0   // tiled DP above this K (all K since the push-style phase B)
 #endif
 // G = DPs per warp: with ALGO_ENVELOPE and small K a warp runs G independent DPs
 // (different gamma) side by side in G lane groups of 32/G lanes, so every
