@@ -41,7 +41,7 @@ int fail(int code, const char* msg)
 }
 
 #ifndef SDEDGE_WARPS
-#define SDEDGE_WARPS 2
+#define SDEDGE_WARPS 1
 #endif
 constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_G
@@ -97,6 +97,7 @@ struct WorkCount {
 };
 
 struct Work {
+    short* S;                      // [grid][ng][K] boundaries j* (1-based), one block per CTA
     unsigned long long* next;      // [2] scenario queue heads (main, big)
     unsigned int* ovf_count;       // scenarios handed to the big-pool pass
     long long* ovf_list;           // [n]
@@ -383,7 +384,6 @@ struct Smem {
     short* jlo;    // [K] first feasible j of row i (memory window), > i if none
     short* jf;     // [K] fixed-plan policies: start j of the batch ending at row i, 0 if none
     short* jw;     // [kWarps][K] heuristic batching: the plan under evaluation
-    short* S;      // [ng][K] boundaries (1-based j*)
     double* tinf;  // [ng]
     double* red;   // [2 * kWarps]
     int* ctl;      // [0] gamma queue, [2] M, [3] bad flag
@@ -409,7 +409,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, in
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
-    b += (size_t)(ng + 2 + kWarps) * K * sizeof(short);
+    b += (size_t)(2 + kWarps) * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
@@ -428,7 +428,6 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jf = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jw = reinterpret_cast<short*>(base + b); b += (size_t)kWarps * K * sizeof(short);
-    s.S = reinterpret_cast<short*>(base + b); b += (size_t)ng * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
     s.red = reinterpret_cast<double*>(base + b); b += 2 * kWarps * sizeof(double);
@@ -1119,7 +1118,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
 
 // ------------------------------------------------------------ the fused kernel
 #ifndef SDEDGE_MINB
-#define SDEDGE_MINB 8     // min resident CTAs per SM requested from ptxas (128-register cap)
+#define SDEDGE_MINB 16    // min resident CTAs per SM requested from ptxas (128-register cap)
 #endif
 
 template <typename R, int ALGO, int RSMEM, int G, int TILE>
@@ -1159,6 +1158,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     }
     unsigned bar_phase = 0u;                  // parity of each staging mbarrier (bit b)
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
+    short* Scta = ws.S + (size_t)blockIdx.x * ng * K;   // this CTA's S vectors (global, L2 resident)
     __shared__ bool s_ovf;
     __shared__ unsigned long long s_work[4];
     __shared__ long long s_top[kWarps * G];
@@ -1268,7 +1268,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 const bool active = gi < ng;       // an idle group repeats gi0 without writing
                 if (!active) gi = gi0;
                 bool ovf = false;
-                short* Sg = active ? sm.S + (size_t)gi * K : nullptr;
+                short* Sg = active ? Scta + (size_t)gi * K : nullptr;
                 const short* jf = (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX)
                                       ? sm.jf : nullptr;
                 double t = 0.0;
@@ -1341,7 +1341,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             }
             double* lat = out.lat + 3 * s;
             if (st == 0) {
-                const short* S = sm.S + (size_t)gbest * K;
+                const short* S = Scta + (size_t)gbest * K;
                 int i = K;
                 while (i > 0) { sm.I[M++] = i; i = S[i - 1] - 1; }   // reuse sm.I as a stack
                 lat[0] = Tcom + best; lat[1] = Tcom; lat[2] = best;
@@ -1600,6 +1600,7 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
     const size_t o_next = take(2 * sizeof(unsigned long long) + sizeof(unsigned int));
+    const size_t o_S = take((size_t)std::max(grid, grid_big) * C.ng * C.K * sizeof(short));
     const size_t o_list = take((size_t)n * sizeof(long long));
     const size_t o_rows = take(C.rows_in_smem ? 0 : (size_t)std::max(slots, slots_big) * C.rows_stride);
     const size_t o_pool = take((size_t)slots * pool_bytes<R>(cap_main));
@@ -1609,6 +1610,7 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     CU(cudaMemsetAsync(wsb + o_next, 0, 2 * sizeof(unsigned long long) + sizeof(unsigned int), st));
 
     Work w;
+    w.S = reinterpret_cast<short*>(wsb + o_S);
     w.next = reinterpret_cast<unsigned long long*>(wsb + o_next);
     w.ovf_count = reinterpret_cast<unsigned int*>(wsb + o_next + 2 * sizeof(unsigned long long));
     w.ovf_list = reinterpret_cast<long long*>(wsb + o_list);
