@@ -40,12 +40,12 @@ FP32_LANES_PER_SM = 128
 # Algorithmic FP64 operations:
 #  dense    4 per candidate-step (n >= 2): Td fma, +Upsilon0 (folded), max, accumulate
 #           -> SURVEY 8(d): 4 W;  plus the per-candidate constant terms.
-#  envelope per candidate 16 (stage-time constants, n = 1 term, verify closed form,
-#           compare), per (candidate, predecessor segment) 10 (two end values,
-#           sign tests, trapezoid sum, accumulate), per DP row 40 (row constants,
-#           argmin, envelope update).
-OPS = {"dense": dict(cand=16, seg=0, step=4, row=40),
-       "envelope": dict(cand=16, seg=10, step=0, row=40)}
+#  envelope per fully evaluated candidate 16 (stage-time constants, n = 1 term,
+#           verify closed form, compare), per (candidate, predecessor segment) 10
+#           (two end values, sign tests, trapezoid sum, accumulate), per pruned
+#           candidate 3 (the lower bound: add, FMA, compare), per DP row 40.
+OPS = {"dense": dict(cand=16, seg=0, step=4, row=40, pruned=0),
+       "envelope": dict(cand=16, seg=10, step=0, row=40, pruned=3)}
 
 # DRAM bytes (read + write) per scenario of the envelope kernel from the one
 # `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_tiled_c4.md:
@@ -245,7 +245,7 @@ def main():
     host = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).pin_memory() for k in ("I", "p", "g", "alpha")}
     d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
     stream = torch.cuda.current_stream(dev)
-    work = torch.zeros(4, dtype=torch.int64, device=dev)
+    work = torch.zeros(5, dtype=torch.int64, device=dev)
     out = sd._alloc_out(torch, n, K, dev, True)
 
     def step(count=False):
@@ -313,7 +313,8 @@ def main():
     lanes = FP64_LANES_PER_SM if prec == 0 else FP32_LANES_PER_SM
     peak = nsm * lanes * 1965e6
     o = OPS[args.algo]
-    ops = o["cand"] * wk[0] + o["seg"] * wk[1] + o["step"] * wk[2] + o["row"] * wk[3]
+    ops = (o["cand"] * wk[4] + o["seg"] * wk[1] + o["step"] * wk[2] + o["row"] * wk[3]
+           + o["pruned"] * (wk[0] - wk[4]))
     t_launch = el / args.steps
     achieved = ops / t_launch
     clocks = clk.summary()
@@ -355,8 +356,9 @@ def main():
                          "traffic_unit": "DRAM bytes per launch (r01 ncu capture, per-scenario scaled)",
                          "algorithmic_bytes": (20 * K + 8 + 36 + 16 * K) * n,
                          "peak_source": f"derived: {nsm} SMs x {lanes} lanes x 1965 MHz (B200_PROFILING.md)",
-                         "work_per_launch": {"candidates": wk[0], "cand_segments": wk[1],
-                                             "candidate_steps_W": wk[2], "rows": wk[3], "ops": ops},
+                         "work_per_launch": {"candidates": wk[0], "full_evaluations": wk[4],
+                                             "cand_segments": wk[1], "candidate_steps_W": wk[2],
+                                             "rows": wk[3], "ops": ops},
                          "kernel": "solve_kernel (main pass)"},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -125,10 +125,11 @@ typedef struct {
     int32_t* order;              /* [n*K] original task index at each sorted position        */
     double*  bw_share;           /* [n*K] w*_k in ORIGINAL task order, or NULL               */
     int32_t* status;             /* [n]                                                      */
-    uint64_t* work_counters;     /* optional DEVICE [4], accumulated (caller zeroes): candidates
-                                    (i,j) evaluated, candidates x predecessor-envelope segments,
-                                    candidate-steps sum N (the paper's O(K^2 N) work W), DP rows;
-                                    NULL = not counted.  Ignored by the _host entry point.     */
+    uint64_t* work_counters;     /* optional DEVICE [5], accumulated (caller zeroes): candidates
+                                    (i,j) considered, fully-evaluated candidates x predecessor-envelope
+                                    segments, candidate-steps sum N (the paper's O(K^2 N) work W),
+                                    DP rows, candidates fully evaluated (the rest were pruned by the
+                                    exact lower bound); NULL = not counted.  Ignored by _host.      */
 } sdedge_schedule;
 
 /* Solve n scenarios.  out_latency: [n*3] = {T, T_com, T_inf} (seconds). */

@@ -88,12 +88,12 @@ struct Outputs {
     int32_t* order;
     double* w;
     int32_t* status;
-    unsigned long long* work;   // [4] or null: candidates, candidate x segments, candidate-steps, rows
+    unsigned long long* work;   // [5] or null: candidates, candidate x segments, candidate-steps, rows, full evals
 };
 
 // Work actually evaluated by one lane (reduced per CTA, flushed once at exit).
 struct WorkCount {
-    unsigned long long cand = 0, seg = 0, steps = 0, rows = 0;
+    unsigned long long cand = 0, seg = 0, steps = 0, rows = 0, full = 0;
 };
 
 struct Work {
@@ -330,6 +330,7 @@ struct RowCoef {
     double td1, ad;       // draft: n = 1 value, n >= 2 intercept            (x b, + c2dg)
     double tv1, av;       // verify: n = 1 value, n >= 2 intercept           (x b, + c2vv)
     double tvb, tvc;      // sum_{n>=2} T^v_n = b tvb + tvc  (closed form, hoisted)
+    double vsl, vc;       // total verify time sum_{n>=1} T^v_n = b vsl + vc (the pruning bound)
 };
 
 __device__ inline RowCoef row_coef(const DPConst& D, int I)
@@ -348,6 +349,8 @@ __device__ inline RowCoef row_coef(const DPConst& D, int I)
     r.av = D.kv * (1.0 + D.g) * vI;
     r.tvb = fma(D.bvc, D.sumM, r.av * D.Mx);
     r.tvc = D.c2vv * D.Mx;
+    r.vsl = r.tv1 + r.tvb;
+    r.vc = D.c2vv + r.tvc;
     return r;
 }
 
@@ -764,6 +767,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
     if (active) {
         wc.cand += n_cand;
+        wc.full += n_cand;
         wc.seg += n_seg;
         wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
         if (gl == 0) wc.rows += rows_done;
@@ -813,6 +817,24 @@ __device__ inline void fence_proxy_async_global()
 }
 
 // ------------------------------------------------------------ tiled DP (large K)
+// Exact pruning: T_{i,j} = Upsilon[p,0,0] + sum_n T^v_n(b) + [max(y0 + T^d_1 - y1, 0)
+// + positive part of the envelope sum] >= LB = (y1[p] + es[p]) + (b vsl + vc).  A candidate whose LB
+// exceeds the row's running best by more than any rounding (relative 1e-13) can neither win nor tie,
+// so its full evaluation is skipped; the decisions are the same as without pruning.
+#ifndef SDEDGE_PRUNE
+#define SDEDGE_PRUNE 1
+#endif
+template <typename R>
+__device__ inline bool prunable(const RowRec<R>* q, const RowCoef& rc, double bd, R bT)
+{
+#if SDEDGE_PRUNE
+    const R lb = (q->Y.y + q->E.x) + (R)fma(bd, rc.vsl, rc.vc);
+    return lb > bT * (R)(1.0 + 1e-13);
+#else
+    return false;
+#endif
+}
+
 // Record-pointer versions of the segment walk, candidate and update (the
 // predecessor may live in global memory or in the shared tile buffer).
 template <typename R>
@@ -1008,7 +1030,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     if (gl == 0) *Ds = Dl;
     __syncwarp();
     const DPConst& D = *Ds;
-    unsigned n_cand = 0, n_seg = 0;
+    unsigned n_cand = 0, n_seg = 0, n_full = 0;
     if (gl == 0) {                           // row 0 == 0 (reading A3); empty segment pool
         *top_s = 0;
         rw[0].Y = R2<R>{(R)0, (R)0};
@@ -1058,11 +1080,14 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             const int a = p0 + c * kTileCh, e = min(a + kTileCh, i0);
             const RowRec<R>* buf = stage + (c & 1) * (kTileCh + 1) + (a % ALN);
             for (int p = a; p < e; ++p, bd -= 1.0) {
-                R r0;
-                int c0;
-                const R T0 = env_cand_rec(buf + (p - a), pl, D, rc, bd, Mx, r0, c0);
-                if (own && p + 1 >= jlo_i) {
-                    n_cand += 1;
+                const RowRec<R>* q = buf + (p - a);
+                const bool cand = own && p + 1 >= jlo_i;
+                n_cand += cand;
+                if (cand && !prunable(q, rc, bd, bT)) {
+                    R r0;
+                    int c0;
+                    const R T0 = env_cand_rec(q, pl, D, rc, bd, Mx, r0, c0);
+                    n_full += 1;
                     n_seg += (unsigned)c0;
                     if (T0 <= bT) { bT = T0; bj = p + 1; brest = r0; }   // ascending j: '<=' keeps the largest
                 }
@@ -1089,12 +1114,15 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             }
             __syncwarp();
             if (own && gl > r && ii + 1 >= jlo_i) {   // candidate j = ii+1 of the later rows
-                R rq;
-                int c0;
-                const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
                 n_cand += 1;
-                n_seg += (unsigned)c0;
-                if (t <= bT) { bT = t; bj = ii + 1; brest = rq; }   // ascending j: '<=' keeps the largest
+                if (!prunable(tb + r, rc, (double)(i - ii), bT)) {
+                    R rq;
+                    int c0;
+                    const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
+                    n_full += 1;
+                    n_seg += (unsigned)c0;
+                    if (t <= bT) { bT = t; bj = ii + 1; brest = rq; }   // ascending j: '<=' keeps the largest
+                }
             }
             ++rows_done;
         }
@@ -1110,6 +1138,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     if (active) {
         wc.cand += n_cand;
         wc.seg += n_seg;
+        wc.full += n_full;
         wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
         if (gl == 0) wc.rows += rows_done;
     }
@@ -1160,9 +1189,9 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     short* Scta = ws.S + (size_t)blockIdx.x * ng * K;   // this CTA's S vectors (global, L2 resident)
     __shared__ bool s_ovf;
-    __shared__ unsigned long long s_work[4];
+    __shared__ unsigned long long s_work[5];
     __shared__ long long s_top[kWarps * G];
-    if (tid < 4) s_work[tid] = 0;
+    if (tid < 5) s_work[tid] = 0;
     WorkCount wc;
 
     for (;;) {
@@ -1376,13 +1405,13 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         __syncthreads();
     }
     if (out.work) {
-        unsigned long long v[4] = {wc.cand, wc.seg, wc.steps, wc.rows};
-        for (int q = 0; q < 4; ++q) {
+        unsigned long long v[5] = {wc.cand, wc.seg, wc.steps, wc.rows, wc.full};
+        for (int q = 0; q < 5; ++q) {
             for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
             if (lane == 0) atomicAdd(&s_work[q], v[q]);
         }
         __syncthreads();
-        if (tid < 4) atomicAdd(out.work + tid, s_work[tid]);
+        if (tid < 5) atomicAdd(out.work + tid, s_work[tid]);
     }
 }
 
