@@ -48,11 +48,11 @@ OPS = {"dense": dict(cand=16, seg=0, step=4, row=40, pruned=0),
        "envelope": dict(cand=16, seg=10, step=0, row=40, pruned=3)}
 
 # DRAM bytes (read + write) per scenario of the envelope kernel from the one
-# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_tiled_c4.md:
-# 2.06 GB read + 14.69 GB written for a 1e5-scenario C4 launch), scaled to the
+# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_final_c4.md:
+# 5.42 GB read + 14.80 GB written for a 1e5-scenario C4 launch), scaled to the
 # launch.  The algorithmic bytes are 2568 in + 2084 out per scenario; the rest
 # is the write-back of the tiled DP's global row store.
-NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (2.060626e9 + 14.687073e9) / 1e5}
+NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (5.423318e9 + 14.795916e9) / 1e5}
 
 
 def parse():
@@ -323,7 +323,7 @@ def main():
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            m = args.cpu_sample or cores
+            m = args.cpu_sample or 3 * cores   # ~15 s of oracle work on the box
             try:
                 r, tt = oracle_rate(pd, {k: (v[:m] if v is not None else None) for k, v in sc.items()}, cores)
                 cpu = {"value": r, "unit": "scenarios/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
