@@ -121,6 +121,7 @@ struct alignas(16) RowRec {                  // 80 B (fp64) / 48 B (fp32): 16-by
     R2<R> E;           // (sum_{n=2}^{N} Upsilon[p,n,1], last m of the first envelope segment)
     R2<R> Ln;          // first envelope segment's line (intercept, slope in m = n-1)
     int cnt, off;      // #segments; extra segments in pool[off .. off+cnt-2]
+    R key;             // Y.y + E.x = Upsilon[p,0,0] (tiled DP: the pruning bound's predecessor term)
 };
 
 template <typename R>
@@ -819,21 +820,31 @@ __device__ inline void fence_proxy_async_global()
 // ------------------------------------------------------------ tiled DP (large K)
 // Exact pruning: T_{i,j} = Upsilon[p,0,0] + sum_n T^v_n(b) + [max(y0 + T^d_1 - y1, 0)
 // + positive part of the envelope sum] >= LB = (y1[p] + es[p]) + (b vsl + vc).  A candidate whose LB
-// exceeds the row's running best by more than any rounding (relative 1e-13) can neither win nor tie,
+// exceeds the row's running best by more than any rounding (relative 1e-13, fp32 1e-6) can neither win nor tie,
 // so its full evaluation is skipped; the decisions are the same as without pruning.
 #ifndef SDEDGE_PRUNE
 #define SDEDGE_PRUNE 1
 #endif
+#ifndef SDEDGE_GUESS
+#define SDEDGE_GUESS 1     // warm start: bit 0 same batch start, bit 1 same batch size as row i0-1
+#endif
+// thr = bT (1 + 1e-13), kept next to the running best bT.
 template <typename R>
-__device__ inline bool prunable(const RowRec<R>* q, const RowCoef& rc, double bd, R bT)
+__device__ inline R prune_lb(const RowRec<R>* q, const RowCoef& rc, double bd)
+{
+    return q->key + (R)fma(bd, rc.vsl, rc.vc);
+}
+template <typename R>
+__device__ inline bool prunable(const RowRec<R>* q, const RowCoef& rc, double bd, R thr)
 {
 #if SDEDGE_PRUNE
-    const R lb = (q->Y.y + q->E.x) + (R)fma(bd, rc.vsl, rc.vc);
-    return lb > bT * (R)(1.0 + 1e-13);
+    return prune_lb(q, rc, bd) > thr;
 #else
     return false;
 #endif
 }
+// (fp32: the margin must exceed a few float roundings; 1 + 1e-13 would round to 1)
+template <typename R> __device__ inline R prune_thr(R bT) { return bT * (sizeof(R) == 8 ? (R)(1.0 + 1e-13) : (R)(1.0 + 1e-6)); }
 
 // Record-pointer versions of the segment walk, candidate and update (the
 // predecessor may live in global memory or in the shared tile buffer).
@@ -974,8 +985,9 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_
         const R2<R> Ln = cntp == 0 ? R2<R>{(R)0, (R)0}
                                    : (pu ? R2<R>{P + Av, Q + Bv} : R2<R>{ln.x + Av, ln.y + Bv});
         const R2<R> E{rest, cntp == 0 ? (R)0 : (R)Mx};
-        o_s->Y = Y; o_s->A = A; o_s->E = E; o_s->Ln = Ln; o_s->cnt = cntp; o_s->off = 0;
-        o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0;
+        const R key = d1 + rest;
+        o_s->Y = Y; o_s->A = A; o_s->E = E; o_s->Ln = Ln; o_s->cnt = cntp; o_s->off = 0; o_s->key = key;
+        o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0; o_g->key = key;
         return false;
     }
     long long top = *top_s;
@@ -983,6 +995,7 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_
     o_s->A = A;
     o_s->off = (int)top;
     const bool ovf = row_merge_rec(q, o_s, pl, P, Q, Av, Bv, rest, Mx, top);
+    o_s->key = d1 + rest;
     *top_s = top;
     *o_g = *o_s;
     return ovf;
@@ -1039,12 +1052,14 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         rw[0].Ln = R2<R>{(R)0, (R)0};
         rw[0].off = 0;
         rw[0].cnt = Mx >= 1 ? 1 : 0;
+        rw[0].key = (R)0;
         fence_proxy_async_global();
     }
     __syncwarp();
     int rows_done = 0;
     bool ovf_any = false, infeasible = false;
     R t_row = (R)0;                          // Upsilon[i,0,0] of the last row this lane finalized
+    int jprev = 0;                           // j* of row i0-1 (the previous tile's last row)
     for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
         const int i = i0 + gl;               // this lane's row
         const bool own = i <= K;
@@ -1052,44 +1067,92 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         RowCoef rc{};
         if (own) rc = row_coef(D, sm.Is[i - 1]);
         // ---- phase A: predecessors p < i0 (final rows, global store)
-        R bT = kinf<R>();
+        R bT = kinf<R>(), thr = kinf<R>();
         int bj = -1;
         R brest = (R)0;
         const int pA = __reduce_min_sync(0xffffffffu, jlo_i) - 1;   // jlo is gamma-independent
         const int p0 = max(pA, 0);
-        double bd = (double)(i - p0);
+        const int pst = own ? jlo_i - 1 : K + 1;                    // this lane's first predecessor
         // Predecessor rows p0 .. i0-1 stream through two shared staging buffers by
         // TMA bulk copies (cp.async.bulk + mbarrier): chunk c+1 is in flight while
         // chunk c is consumed with broadcast shared loads.
         static_assert(sizeof(RowRec<R>) % 16 == 0, "TMA bulk copies need 16-byte multiples");
-        constexpr int ALN = 1;
+        static_assert(kTileCh <= 32, "chunk masks are 32-bit");
         const int nrows = i0 - p0;
         const int nch = (nrows + kTileCh - 1) / kTileCh;
         if (gl == 0 && nch > 0) {
-            const int e = min(p0 + kTileCh, i0), a16 = p0 - p0 % ALN;   // 16-byte aligned global start
-            bulk_load(stage, rw + a16, (unsigned)((e - a16) * sizeof(RowRec<R>)), bars);
+            const int e = min(p0 + kTileCh, i0);
+            bulk_load(stage, rw + p0, (unsigned)((e - p0) * sizeof(RowRec<R>)), bars);
         }
+        // Warm start: before the scan, evaluate the candidate(s)
+        // suggested by the previous row's winner -- the same batch start and/or the
+        // same batch size -- so that the threshold is tight from the first
+        // predecessor on.  Ties are then broken explicitly (largest j wins).
+        int pg1 = -1, pg2 = -1;
+#if SDEDGE_GUESS
+        if (jprev > 0 && own) {
+            const int jlo_c = max(jlo_i, 1);
+            if (SDEDGE_GUESS & 1) pg1 = min(max(jprev, jlo_c), i0) - 1;                  // same start
+            if (SDEDGE_GUESS & 2) pg2 = min(max(i - i0 + jprev + 1, jlo_c), i0) - 1;     // same size
+            if (pg2 == pg1) pg2 = -1;
+#pragma unroll 1
+            for (int t = 0; t < 2; ++t) {
+                const int pg = t ? pg2 : pg1;
+                if (pg < 0) continue;
+                R r0;
+                int c0;
+                const double bd = (double)(i - pg);
+                const R T0 = env_cand_rec(rw + pg, pl, D, rc, bd, Mx, r0, c0);
+                n_full += 1;
+                n_seg += (unsigned)c0;
+                if (T0 < bT || (T0 == bT && pg + 1 > bj)) { bT = T0; thr = prune_thr(bT); bj = pg + 1; brest = r0; }
+            }
+        }
+#endif
         for (int c = 0; c < nch; ++c) {
             if (gl == 0 && c + 1 < nch) {
-                const int a1 = p0 + (c + 1) * kTileCh, e1 = min(a1 + kTileCh, i0), a16 = a1 - a1 % ALN;
-                bulk_load(stage + ((c + 1) & 1) * (kTileCh + 1), rw + a16,
-                          (unsigned)((e1 - a16) * sizeof(RowRec<R>)), bars + ((c + 1) & 1));
+                const int a1 = p0 + (c + 1) * kTileCh, e1 = min(a1 + kTileCh, i0);
+                bulk_load(stage + ((c + 1) & 1) * (kTileCh + 1), rw + a1,
+                          (unsigned)((e1 - a1) * sizeof(RowRec<R>)), bars + ((c + 1) & 1));
             }
             mbar_wait(bars + (c & 1), (bar_phase >> (c & 1)) & 1u);
             bar_phase ^= 1u << (c & 1);
             const int a = p0 + c * kTileCh, e = min(a + kTileCh, i0);
-            const RowRec<R>* buf = stage + (c & 1) * (kTileCh + 1) + (a % ALN);
-            for (int p = a; p < e; ++p, bd -= 1.0) {
-                const RowRec<R>* q = buf + (p - a);
-                const bool cand = own && p + 1 >= jlo_i;
-                n_cand += cand;
-                if (cand && !prunable(q, rc, bd, bT)) {
+            const RowRec<R>* buf = stage + (c & 1) * (kTileCh + 1);
+            const double bda = (double)(i - a);
+            // this lane's candidates in the chunk: predecessors max(a, pst) .. e-1
+            const int lo = max(pst - a, 0), hi = e - a;
+            n_cand += (unsigned)max(hi - lo, 0);
+            // pass 1 (independent, unrolled): the bound of every predecessor of the
+            // chunk against the threshold at the chunk's start -- a superset of the
+            // survivors, since the threshold only falls
+            unsigned m = 0;
+#pragma unroll
+            for (int k = 0; k < kTileCh; ++k)
+                m |= (unsigned)!(prunable(buf + k, rc, bda - (double)k, thr)) << k;
+            m &= lo >= hi ? 0u : (((hi >= 32 ? 0u : (1u << hi)) - 1u) & ~((1u << lo) - 1u));
+#if SDEDGE_GUESS
+            if (pg1 >= a && pg1 < e) m &= ~(1u << (pg1 - a));                 // already evaluated
+            if (pg2 >= a && pg2 < e) m &= ~(1u << (pg2 - a));
+#endif
+            // pass 2: the survivors in ascending j, re-tested against the current
+            // threshold (lanes of the warp evaluate different predecessors together)
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                const double bd = bda - (double)k;
+                const RowRec<R>* q = buf + k;
+                if (!prunable(q, rc, bd, thr)) {
                     R r0;
                     int c0;
                     const R T0 = env_cand_rec(q, pl, D, rc, bd, Mx, r0, c0);
                     n_full += 1;
                     n_seg += (unsigned)c0;
-                    if (T0 <= bT) { bT = T0; bj = p + 1; brest = r0; }   // ascending j: '<=' keeps the largest
+#if SDEDGE_GUESS
+                    if (T0 < bT || (T0 == bT && a + k + 1 > bj)) { bT = T0; thr = prune_thr(bT); bj = a + k + 1; brest = r0; }
+#else
+                    if (T0 <= bT) { bT = T0; thr = prune_thr(bT); bj = a + k + 1; brest = r0; }   // '<=': largest j
+#endif
                 }
             }
             __syncwarp();                                        // buffer (c & 1) may be refilled now
@@ -1115,17 +1178,18 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             __syncwarp();
             if (own && gl > r && ii + 1 >= jlo_i) {   // candidate j = ii+1 of the later rows
                 n_cand += 1;
-                if (!prunable(tb + r, rc, (double)(i - ii), bT)) {
+                if (!prunable(tb + r, rc, (double)(i - ii), thr)) {
                     R rq;
                     int c0;
                     const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
                     n_full += 1;
                     n_seg += (unsigned)c0;
-                    if (t <= bT) { bT = t; bj = ii + 1; brest = rq; }   // ascending j: '<=' keeps the largest
+                    if (t <= bT) { bT = t; thr = prune_thr(bT); bj = ii + 1; brest = rq; }   // '<=': largest j
                 }
             }
             ++rows_done;
         }
+        jprev = __shfl_sync(0xffffffffu, bj, (lane - gl) + GL - 1);
         // later tiles bulk-read this tile's rows through TMA (async proxy): every
         // lane orders the global row stores it made before the next __syncwarp
         fence_proxy_async_global();
