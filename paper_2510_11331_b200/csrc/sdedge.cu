@@ -825,6 +825,12 @@ __device__ inline void fence_proxy_async_global()
 #ifndef SDEDGE_PRUNE
 #define SDEDGE_PRUNE 1
 #endif
+#ifndef SDEDGE_PASS1_FAST
+#define SDEDGE_PASS1_FAST 1  // phase-A bound test as one FMA + compare per predecessor
+#endif
+#ifndef SDEDGE_PREFETCH
+#define SDEDGE_PREFETCH 0  // L1 prefetch of the phase-A winner's record before phase B
+#endif
 #ifndef SDEDGE_GUESS
 #define SDEDGE_GUESS 1     // warm start: bit 0 same batch start, bit 1 same batch size as row i0-1
 #endif
@@ -1127,9 +1133,19 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             // chunk against the threshold at the chunk's start -- a superset of the
             // survivors, since the threshold only falls
             unsigned m = 0;
+#if SDEDGE_PRUNE && SDEDGE_PASS1_FAST
+            // key + (bda - k) vsl + vc > thr  <=>  key > u + k vsl with u = thr - (bda vsl + vc):
+            // two operations per predecessor.  Rounding here is a few ulp of T, far inside the
+            // 1e-13 (fp32: 1e-6) margin of thr, so a pruned candidate still cannot win or tie.
+            const R u = thr - (R)fma(bda, rc.vsl, rc.vc), vs = (R)rc.vsl;
+#pragma unroll
+            for (int k = 0; k < kTileCh; ++k)
+                m |= (unsigned)!(buf[k].key > fma((R)k, vs, u)) << k;
+#else
 #pragma unroll
             for (int k = 0; k < kTileCh; ++k)
                 m |= (unsigned)!(prunable(buf + k, rc, bda - (double)k, thr)) << k;
+#endif
             m &= lo >= hi ? 0u : (((hi >= 32 ? 0u : (1u << hi)) - 1u) & ~((1u << lo) - 1u));
 #if SDEDGE_GUESS
             if (pg1 >= a && pg1 < e) m &= ~(1u << (pg1 - a));                 // already evaluated
@@ -1163,10 +1179,22 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         // tile; each finished row i0+r is "pushed": the later rows of the tile
         // evaluate their candidate with predecessor i0+r (broadcast from the shared
         // tile).  So no reduction is needed: lane r finalizes row i0+r itself.
-        for (int r = 0; r < GL; ++r) {
+#if SDEDGE_PREFETCH
+        // the phase-A winner's record is in the global store (L2): start pulling it
+        // into L1 now, its row update comes up in step gl of the serial phase B
+        if (own && bj > 0) {
+            const char* g = reinterpret_cast<const char*>(rw + (bj - 1));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(g));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(g + sizeof(RowRec<R>) - 1));
+        }
+#endif
+        // rows of the tile up to the first one whose memory window is empty (the
+        // window is gamma-independent, so every group stops at the same row)
+        const unsigned bad_rows = __ballot_sync(0xffffffffu, own && jlo_i > i) & ((GL == 32 ? 0u : (1u << GL)) - 1u);
+        const int rend = min(bad_rows ? __ffs(bad_rows) - 1 : GL, K - i0 + 1);
+        if (bad_rows && __ffs(bad_rows) - 1 < K - i0 + 1) infeasible = true;
+        for (int r = 0; r < rend; ++r) {
             const int ii = i0 + r;
-            if (ii > K) break;
-            if (sm.jlo[ii - 1] > ii) { infeasible = true; break; }   // empty window (uniform)
             if (gl == r) {                   // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
                 if (S) S[ii - 1] = (short)bj;
                 const int p = bj - 1;
