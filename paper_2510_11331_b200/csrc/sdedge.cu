@@ -828,6 +828,9 @@ __device__ inline void fence_proxy_async_global()
 #ifndef SDEDGE_PASS1_FAST
 #define SDEDGE_PASS1_FAST 1  // phase-A bound test as one FMA + compare per predecessor
 #endif
+#ifndef SDEDGE_SPEC
+#define SDEDGE_SPEC 1      // phase B: all rows of a tile built at once from their phase-A winners
+#endif
 #ifndef SDEDGE_PREFETCH
 #define SDEDGE_PREFETCH 0  // L1 prefetch of the phase-A winner's record before phase B
 #endif
@@ -973,10 +976,12 @@ __device__ __noinline__ bool row_merge_rec(const RowRec<R>* q, RowRec<R>* o, con
 // Row i from predecessor record q and the winning candidate (eq:tt1, eq:tt2),
 // stored to the shared tile slot o_s and the global row store o_g; the pool
 // pointer lives in shared memory (only the rare merge path moves it).
-// Returns true on pool overflow.
+// Returns 1 on pool overflow, 2 if `spec` and the row needs the merge path
+// (nothing stored: the pool is allocated in row order, serially), else 0.
 template <typename R>
-__device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g, const Pool<R>& pl,
-                               const DPConst& D, const RowCoef& rc, double bd, R rest, int Mx, long long* top_s)
+__device__ int row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g, const Pool<R>& pl,
+                              const DPConst& D, const RowCoef& rc, double bd, R rest, int Mx, long long* top_s,
+                              bool spec = false)
 {
     const R2<R> y = q->Y, a = q->A, ln = q->Ln;
     const int cntp = q->cnt;
@@ -994,8 +999,9 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_
         const R key = d1 + rest;
         o_s->Y = Y; o_s->A = A; o_s->E = E; o_s->Ln = Ln; o_s->cnt = cntp; o_s->off = 0; o_s->key = key;
         o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0; o_g->key = key;
-        return false;
+        return 0;
     }
+    if (spec) return 2;
     long long top = *top_s;
     o_s->Y = Y;
     o_s->A = A;
@@ -1004,7 +1010,7 @@ __device__ bool row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_
     o_s->key = d1 + rest;
     *top_s = top;
     *o_g = *o_s;
-    return ovf;
+    return ovf ? 1 : 0;
 }
 
 // Algorithm 1 in tiles of GL rows; lane r of a group owns row i0+r throughout.
@@ -1193,13 +1199,53 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         const unsigned bad_rows = __ballot_sync(0xffffffffu, own && jlo_i > i) & ((GL == 32 ? 0u : (1u << GL)) - 1u);
         const int rend = min(bad_rows ? __ffs(bad_rows) - 1 : GL, K - i0 + 1);
         if (bad_rows && __ffs(bad_rows) - 1 < K - i0 + 1) infeasible = true;
+#if SDEDGE_SPEC
+        // Speculation: every lane builds its row from its phase-A winner at once (the
+        // predecessor is a finished row, p < i0).  The serial steps below then only
+        // test the pushed candidates; a lane rebuilds its row in its own step if one
+        // of them won, or if its row needs the merge path (pool space is taken in
+        // row order).  Same candidates, comparisons and tie rule as the serial form.
+        bool fin = false;                    // slot gl holds the row for the current bj
+        if (own && gl < rend && bj > 0) {
+            const int p = bj - 1;
+            fin = row_update_rec(rw + p, tb + gl, rw + i, pl, D, rc, (double)(i - p), brest, Mx, top_s, true) == 0;
+        }
+        __syncwarp();
+        for (int r = 0; r < rend; ++r) {
+            const int ii = i0 + r;
+            if (gl == r && !fin) {           // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
+                const int p = bj - 1;
+                const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
+                if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s) == 1)
+                    ovf_any = true;
+                fin = true;
+            }
+            __syncwarp();
+            if (own && gl > r && ii + 1 >= jlo_i) {   // candidate j = ii+1 of the later rows
+                n_cand += 1;
+                if (!prunable(tb + r, rc, (double)(i - ii), thr)) {
+                    R rq;
+                    int c0;
+                    const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
+                    n_full += 1;
+                    n_seg += (unsigned)c0;
+                    if (t <= bT) { bT = t; thr = prune_thr(bT); bj = ii + 1; brest = rq; fin = false; }   // '<=': largest j
+                }
+            }
+            ++rows_done;
+        }
+        if (own && gl < rend) {
+            if (S) S[i - 1] = (short)bj;
+            t_row = bT;
+        }
+#else
         for (int r = 0; r < rend; ++r) {
             const int ii = i0 + r;
             if (gl == r) {                   // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
                 if (S) S[ii - 1] = (short)bj;
                 const int p = bj - 1;
                 const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
-                if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s))
+                if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s) == 1)
                     ovf_any = true;
                 t_row = bT;
             }
@@ -1217,6 +1263,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             }
             ++rows_done;
         }
+#endif
         jprev = __shfl_sync(0xffffffffu, bj, (lane - gl) + GL - 1);
         // later tiles bulk-read this tile's rows through TMA (async proxy): every
         // lane orders the global row stores it made before the next __syncwarp
