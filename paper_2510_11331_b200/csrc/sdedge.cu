@@ -45,7 +45,7 @@ int fail(int code, const char* msg)
 #endif
 constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_G
-#define SDEDGE_TILE_G 4       // DPs per warp of the tiled DP (tile = 32 / G rows)
+#define SDEDGE_TILE_G 2       // DPs per warp of the tiled DP (tile = 32 / G rows)
 #endif
 #ifndef SDEDGE_TILE_SHFL_ARGMIN
 #define SDEDGE_TILE_SHFL_ARGMIN 1
@@ -396,7 +396,7 @@ struct Smem {
 };
 
 #ifndef SDEDGE_TILE_CH
-#define SDEDGE_TILE_CH 8      // rows per TMA chunk of the tiled DP's phase A
+#define SDEDGE_TILE_CH 16     // rows per TMA chunk of the tiled DP's phase A
 #endif
 constexpr int kTileCh = SDEDGE_TILE_CH;
 
@@ -405,7 +405,7 @@ template <typename R, int G>
 __host__ __device__ inline size_t tile_bytes()
 {
     return (size_t)(32 / G) * sizeof(RowRec<R>) +
-           2 * (size_t)(kTileCh + 1) * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
+           2 * (size_t)kTileCh * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
 }
 
 template <typename R, int G>
@@ -801,6 +801,27 @@ __device__ inline void bulk_load(void* dst, const void* src, unsigned bytes, uns
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// The same chunk of rows for all G DPs of the warp, issued by one lane: DP g's
+// staging buffer b is at st0 + g tstride + b kTileCh sizeof(RowRec), its
+// mbarriers right after the two buffers, its row store at rw0 + g rwstride.  All
+// operands are warp-uniform, so the copies need no per-lane serialisation.
+template <typename R, int G>
+__device__ inline void bulk_load_groups(unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
+                                        int a, unsigned bytes, int b)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const unsigned st = st0 + (unsigned)g * tstride;
+        const unsigned bar = st + 2u * kTileCh * (unsigned)sizeof(RowRec<R>) + 8u * (unsigned)b;
+        const unsigned dst = st + (unsigned)b * kTileCh * (unsigned)sizeof(RowRec<R>);
+        const unsigned char* src = rw0 + g * rwstride + (long long)a * (long long)sizeof(RowRec<R>);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+    }
+}
+
 __device__ inline void mbar_wait(unsigned long long* bar, unsigned phase)
 {
     unsigned done = 0;
@@ -828,6 +849,12 @@ __device__ inline void fence_proxy_async_global()
 #ifndef SDEDGE_PASS1_FAST
 #define SDEDGE_PASS1_FAST 1  // phase-A bound test as one FMA + compare per predecessor
 #endif
+#ifndef SDEDGE_LB2
+#define SDEDGE_LB2 1          // pass 2: the Jensen bound on the envelope sum before a full evaluation
+#endif
+#ifndef SDEDGE_TMA_LANE0
+#define SDEDGE_TMA_LANE0 0    // 1: lane 0 issues the chunk copies of all G DPs (uniform operands)
+#endif
 #ifndef SDEDGE_SPEC
 #define SDEDGE_SPEC 1      // phase B: all rows of a tile built at once from their phase-A winners
 #endif
@@ -853,6 +880,25 @@ __device__ inline bool prunable(const RowRec<R>* q, const RowCoef& rc, double bd
 #endif
 }
 // (fp32: the margin must exceed a few float roundings; 1 + 1e-13 would round to 1)
+// Second bound, for the pass-2 survivors (before the full evaluation): the
+// envelope sum is sum_m max(P + Q m - env_p(m), 0) >= max(Mx P + sumM Q - E.x, 0)
+// (Jensen on the positive part; sum_m env_p(m) = E.x), so T >= LB + that.  The
+// difference of two large sums is taken with a slack of 1e-12 (fp32 1e-5) of
+// their size, far above its rounding, so this too never prunes a winner or tie.
+template <typename R>
+__device__ inline bool prunable2(const RowRec<R>* q, const RowCoef& rc, const DPConst& D, double bd, R lb, R thr)
+{
+#if SDEDGE_PRUNE && SDEDGE_LB2
+    const R P = q->A.x + (R)fma(bd, rc.ad, D.c2dg), Q = q->A.y + (R)(bd * D.bdc);
+    const R ex = q->E.x;
+    const R X = fma((R)D.Mx, P, fma((R)D.sumM, Q, -ex));
+    const R dl = (sizeof(R) == 8 ? (R)1e-12 : (R)1e-5) * (ex + ex + fabs(X));
+    return lb + rmax(X - dl, (R)0) > thr;
+#else
+    return false;
+#endif
+}
+
 template <typename R> __device__ inline R prune_thr(R bT) { return bT * (sizeof(R) == 8 ? (R)(1.0 + 1e-13) : (R)(1.0 + 1e-6)); }
 
 // Record-pointer versions of the segment walk, candidate and update (the
@@ -1025,6 +1071,7 @@ __device__ int row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g
 template <typename R, int G>
 __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, RowRec<R>* tb,
                                  RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
+                                 unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
                                  DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
                                  double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
 {
@@ -1092,9 +1139,13 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         static_assert(kTileCh <= 32, "chunk masks are 32-bit");
         const int nrows = i0 - p0;
         const int nch = (nrows + kTileCh - 1) / kTileCh;
-        if (gl == 0 && nch > 0) {
+        if (nch > 0) {
             const int e = min(p0 + kTileCh, i0);
-            bulk_load(stage, rw + p0, (unsigned)((e - p0) * sizeof(RowRec<R>)), bars);
+#if SDEDGE_TMA_LANE0
+            if (lane == 0) bulk_load_groups<R, G>(st0, tstride, rw0, rwstride, p0, (unsigned)((e - p0) * sizeof(RowRec<R>)), 0);
+#else
+            if (gl == 0) bulk_load(stage, rw + p0, (unsigned)((e - p0) * sizeof(RowRec<R>)), bars);
+#endif
         }
         // Warm start: before the scan, evaluate the candidate(s)
         // suggested by the previous row's winner -- the same batch start and/or the
@@ -1102,7 +1153,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         // predecessor on.  Ties are then broken explicitly (largest j wins).
         int pg1 = -1, pg2 = -1;
 #if SDEDGE_GUESS
-        if (jprev > 0 && own) {
+        if (jprev > 0 && own && pst <= i0 - 1) {   // only if the window reaches before the tile
             const int jlo_c = max(jlo_i, 1);
             if (SDEDGE_GUESS & 1) pg1 = min(max(jprev, jlo_c), i0) - 1;                  // same start
             if (SDEDGE_GUESS & 2) pg2 = min(max(i - i0 + jprev + 1, jlo_c), i0) - 1;     // same size
@@ -1122,15 +1173,22 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         }
 #endif
         for (int c = 0; c < nch; ++c) {
-            if (gl == 0 && c + 1 < nch) {
+            if (c + 1 < nch) {
                 const int a1 = p0 + (c + 1) * kTileCh, e1 = min(a1 + kTileCh, i0);
-                bulk_load(stage + ((c + 1) & 1) * (kTileCh + 1), rw + a1,
-                          (unsigned)((e1 - a1) * sizeof(RowRec<R>)), bars + ((c + 1) & 1));
+#if SDEDGE_TMA_LANE0
+                if (lane == 0)
+                    bulk_load_groups<R, G>(st0, tstride, rw0, rwstride, a1, (unsigned)((e1 - a1) * sizeof(RowRec<R>)),
+                                           (c + 1) & 1);
+#else
+                if (gl == 0)
+                    bulk_load(stage + ((c + 1) & 1) * kTileCh, rw + a1, (unsigned)((e1 - a1) * sizeof(RowRec<R>)),
+                              bars + ((c + 1) & 1));
+#endif
             }
             mbar_wait(bars + (c & 1), (bar_phase >> (c & 1)) & 1u);
             bar_phase ^= 1u << (c & 1);
             const int a = p0 + c * kTileCh, e = min(a + kTileCh, i0);
-            const RowRec<R>* buf = stage + (c & 1) * (kTileCh + 1);
+            const RowRec<R>* buf = stage + (c & 1) * kTileCh;
             const double bda = (double)(i - a);
             // this lane's candidates in the chunk: predecessors max(a, pst) .. e-1
             const int lo = max(pst - a, 0), hi = e - a;
@@ -1152,11 +1210,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             for (int k = 0; k < kTileCh; ++k)
                 m |= (unsigned)!(prunable(buf + k, rc, bda - (double)k, thr)) << k;
 #endif
-            m &= lo >= hi ? 0u : (((hi >= 32 ? 0u : (1u << hi)) - 1u) & ~((1u << lo) - 1u));
-#if SDEDGE_GUESS
-            if (pg1 >= a && pg1 < e) m &= ~(1u << (pg1 - a));                 // already evaluated
-            if (pg2 >= a && pg2 < e) m &= ~(1u << (pg2 - a));
-#endif
+            m &= lo >= kTileCh ? 0u : (0xffffffffu << lo);
+            if (hi < kTileCh) m &= (1u << hi) - 1u;              // the last chunk of the window
             // pass 2: the survivors in ascending j, re-tested against the current
             // threshold (lanes of the warp evaluate different predecessors together)
             while (m) {
@@ -1164,7 +1219,9 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                 m &= m - 1;
                 const double bd = bda - (double)k;
                 const RowRec<R>* q = buf + k;
-                if (!prunable(q, rc, bd, thr)) {
+                const R lb = prune_lb(q, rc, bd);
+                if (!(SDEDGE_PRUNE && lb > thr) && a + k != pg1 && a + k != pg2 &&   // guesses: done
+                    !prunable2(q, rc, D, bd, lb, thr)) {
                     R r0;
                     int c0;
                     const R T0 = env_cand_rec(q, pl, D, rc, bd, Mx, r0, c0);
@@ -1223,7 +1280,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             __syncwarp();
             if (own && gl > r && ii + 1 >= jlo_i) {   // candidate j = ii+1 of the later rows
                 n_cand += 1;
-                if (!prunable(tb + r, rc, (double)(i - ii), thr)) {
+                const R lb = prune_lb(tb + r, rc, (double)(i - ii));
+                if (!(SDEDGE_PRUNE && lb > thr) && !prunable2(tb + r, rc, D, (double)(i - ii), lb, thr)) {
                     R rq;
                     int c0;
                     const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
@@ -1315,7 +1373,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                            (size_t)(warp * G + grp) * tile_bytes<R, G>();
         tb = reinterpret_cast<RowRec<R>*>(t);
         stage = reinterpret_cast<RowRec<R>*>(t + (size_t)GL * sizeof(RowRec<R>));
-        bars = reinterpret_cast<unsigned long long*>(stage + 2 * (kTileCh + 1));
+        bars = reinterpret_cast<unsigned long long*>(stage + 2 * kTileCh);
         dpc = reinterpret_cast<DPConst*>(bars + 2);
         if (lane % GL == 0) {
             mbar_init(bars, 1);
@@ -1325,6 +1383,12 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         __syncwarp();
     }
     unsigned bar_phase = 0u;                  // parity of each staging mbarrier (bit b)
+    // warp-uniform addresses of group 0's staging buffer and row store (TMA issue)
+    const unsigned tb_stride = (unsigned)tile_bytes<R, G>();
+    const int wu = kWarps == 1 ? 0 : warp;
+    const unsigned st0 = TILE ? smem_u32(sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K) : 0) +
+                                         (size_t)(wu * G) * tb_stride) + (unsigned)(GL * sizeof(RowRec<R>)) : 0u;
+    const unsigned char* rw0 = ws.rows + (size_t)((long long)blockIdx.x * kWarps + wu) * G * C.rows_stride;
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     short* Scta = ws.S + (size_t)blockIdx.x * ng * K;   // this CTA's S vectors (global, L2 resident)
     __shared__ bool s_ovf;
@@ -1444,7 +1508,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 // other instantiations compile just their own DP (fewer live registers)
                 constexpr bool kBase = G == 1 && !TILE;
                 if constexpr (TILE) {
-                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, dpc, C.gmin + gi, alpha,
+                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
+                                             C.rows_stride, dpc, C.gmin + gi, alpha,
                                              c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
@@ -1746,7 +1811,9 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
-    auto k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1, G, TILE> : solve_kernel<R, ALGO, 0, G, TILE>;
+    // (the tiled DP keeps its rows in global memory: no RSMEM instantiation for it)
+    auto k_main = (!TILE && C.rows_in_smem) ? solve_kernel<R, ALGO, TILE ? 0 : 1, G, TILE>
+                                            : solve_kernel<R, ALGO, 0, G, TILE>;
     auto k_big = k_main;
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));

@@ -144,6 +144,26 @@ def test_memory_window_and_infeasible():
     assert np.all(np.isinf(g["lat"][g["status"] == 1, 0]))
 
 
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+@pytest.mark.parametrize("bmax", [2, 5, 9, 31])
+def test_narrow_memory_windows(pair, bmax):
+    """Memory windows narrower than a DP tile (Alg. 1 lines 10-13):
+    with b_max < tile rows a row's window starts inside its own tile, so the
+    tiled DP has no older predecessor for it and the warm start must not
+    propose one.  Capacity = weights + b_max KV caches of a mid-length task."""
+    K = 64
+    pd = scengen.params(pair, K=K, gamma_min=1, gamma_max=8)
+    J, h1, h2 = scengen.MODELS[pair.split("-")[0]]
+    cap = oracle.param_memory(J, h1, h2) + bmax * oracle.kv_memory_per_task(J, h1, 256, pd["O_max"])
+    pd = dict(pd, mem_capacity_bytes=int(cap))
+    sc = scengen.generate(40 + bmax, K, 0, 300)
+    for prec in (0, 1):
+        res, orc, g = _check(pd, sc, prec, ENV)
+        assert res["failures"] == 0
+    ends = [np.diff(np.r_[0, g["batch_end"][s][: g["M"][s]]]).max() for s in range(300) if g["status"][s] == 0]
+    assert len(ends) > 0 and max(ends) <= 2 * bmax + 2     # the windows really bind
+
+
 def test_invalid_scenarios_status():
     pd = scengen.params("68M-7B", K=8, gamma_min=1, gamma_max=3)
     sc = scengen.generate(23, 8, 0, 6)
