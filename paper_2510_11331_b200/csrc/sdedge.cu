@@ -856,7 +856,7 @@ __device__ inline void fence_proxy_async_global()
 #define SDEDGE_TMA_LANE0 0    // 1: lane 0 issues the chunk copies of all G DPs (uniform operands)
 #endif
 #ifndef SDEDGE_SPEC
-#define SDEDGE_SPEC 1      // phase B: all rows of a tile built at once from their phase-A winners
+#define SDEDGE_SPEC 2      // phase B: rows built at once from their phase-A winners (2: only the steps that matter run)
 #endif
 #ifndef SDEDGE_PREFETCH
 #define SDEDGE_PREFETCH 0  // L1 prefetch of the phase-A winner's record before phase B
@@ -1268,6 +1268,52 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             fin = row_update_rec(rw + p, tb + gl, rw + i, pl, D, rc, (double)(i - p), brest, Mx, top_s, true) == 0;
         }
         __syncwarp();
+#if SDEDGE_SPEC >= 2
+        // In-tile candidates j = i0+r+1 (predecessor row i0+r, r < gl) are first
+        // tested against the speculative rows, all at once; then only the steps r
+        // that hold a surviving candidate or a row to rebuild run.  A rebuilt row's
+        // candidates are re-tested by every later row (its key may have fallen).
+        const int rlo = max(jlo_i - i0 - 1, 0);          // j = i0+r+1 >= jlo_i
+        const bool live = own && gl < rend;
+        unsigned cm = 0;
+        {
+            const R u = thr - (R)fma((double)(i - i0), rc.vsl, rc.vc), vs = (R)rc.vsl;
+#pragma unroll
+            for (int r = 0; r < GL; ++r) cm |= (unsigned)!(SDEDGE_PRUNE && tb[r].key > fma((R)r, vs, u)) << r;
+            cm &= (live && rlo < gl) ? (((1u << gl) - 1u) & (0xffffffffu << rlo)) : 0u;
+            if (live) n_cand += (unsigned)max(gl - rlo, 0);
+        }
+        unsigned todo = __reduce_or_sync(0xffffffffu, cm | ((live && !fin) ? 1u << gl : 0u));
+        while (todo) {
+            const int r = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int ii = i0 + r;
+            bool rebuilt = false;
+            if (gl == r && !fin) {           // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
+                const int p = bj - 1;
+                const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
+                if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s) == 1)
+                    ovf_any = true;
+                fin = true;
+                rebuilt = true;
+            }
+            __syncwarp();
+            const bool chg = __shfl_sync(0xffffffffu, rebuilt, (lane - gl) + r);
+            if (live && gl > r && r >= rlo && (chg || ((cm >> r) & 1u))) {
+                const R lb = prune_lb(tb + r, rc, (double)(i - ii));
+                if (!(SDEDGE_PRUNE && lb > thr) && !prunable2(tb + r, rc, D, (double)(i - ii), lb, thr)) {
+                    R rq;
+                    int c0;
+                    const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
+                    n_full += 1;
+                    n_seg += (unsigned)c0;
+                    if (t <= bT) { bT = t; thr = prune_thr(bT); bj = ii + 1; brest = rq; fin = false; }   // '<=': largest j
+                }
+            }
+            todo |= __reduce_or_sync(0xffffffffu, (live && !fin) ? 1u << gl : 0u);   // rows that must be rebuilt
+        }
+        rows_done += rend;
+#else
         for (int r = 0; r < rend; ++r) {
             const int ii = i0 + r;
             if (gl == r && !fin) {           // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
@@ -1292,6 +1338,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             }
             ++rows_done;
         }
+#endif
         if (own && gl < rend) {
             if (S) S[i - 1] = (short)bj;
             t_row = bT;
