@@ -849,6 +849,9 @@ __device__ inline void fence_proxy_async_global()
 #ifndef SDEDGE_PASS1_FAST
 #define SDEDGE_PASS1_FAST 1  // phase-A bound test as one FMA + compare per predecessor
 #endif
+#ifndef SDEDGE_GAMMA_ABORT
+#define SDEDGE_GAMMA_ABORT 1  // stop a gamma's DP once its partial optimum exceeds the best finished gamma
+#endif
 #ifndef SDEDGE_LB2
 #define SDEDGE_LB2 1          // pass 2: the Jensen bound on the envelope sum before a full evaluation
 #endif
@@ -1073,7 +1076,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                                  RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
                                  unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
                                  DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
-                                 double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active)
+                                 double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
+                                 const double* best_s)
 {
     constexpr int GL = 32 / G;
     const int lane = threadIdx.x & 31;
@@ -1116,7 +1120,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     }
     __syncwarp();
     int rows_done = 0;
-    bool ovf_any = false, infeasible = false;
+    bool ovf_any = false, infeasible = false, aborted = !active;
     R t_row = (R)0;                          // Upsilon[i,0,0] of the last row this lane finalized
     int jprev = 0;                           // j* of row i0-1 (the previous tile's last row)
     for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
@@ -1374,10 +1378,24 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         // lane orders the global row stores it made before the next __syncwarp
         fence_proxy_async_global();
         __syncwarp();
+#if SDEDGE_GAMMA_ABORT
+        // Exact gamma-level pruning: the optimal latency of the first i tasks is
+        // non-decreasing in i (drop the last task from its batch: the batch shrinks,
+        // its padded length cannot grow, every stage time can only fall), so once
+        // T*(i0+GL-1) exceeds the best T_inf of an already finished gamma, this gamma
+        // cannot win or tie.  Margins cover the rounding of both DPs.
+        if (best_s && rend == GL) {
+            const R kl = __shfl_sync(0xffffffffu, t_row, (lane - gl) + GL - 1);
+            const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
+            aborted |= (double)kl * (1.0 - mg) > *best_s * (1.0 + mg);
+            if (__all_sync(0xffffffffu, aborted)) break;
+        }
+#endif
     }
     // T_inf = Upsilon[K,0,0], held by the lane that finalized row K
     double T_last = (double)__shfl_sync(0xffffffffu, t_row, (lane - gl) + (K - 1) % GL);
     if (infeasible) T_last = dinf();
+    if (aborted) T_last = dinf();            // pruned (or an idle group)
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
     if (active) {
         wc.cand += n_cand;
@@ -1439,6 +1457,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     short* Scta = ws.S + (size_t)blockIdx.x * ng * K;   // this CTA's S vectors (global, L2 resident)
     __shared__ bool s_ovf;
+    __shared__ double s_best;                // best T_inf of the finished gammas of this scenario
     __shared__ unsigned long long s_work[5];
     __shared__ long long s_top[kWarps * G];
     if (tid < 5) s_work[tid] = 0;
@@ -1450,6 +1469,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
             sm.ctl[0] = 0;
             s_ovf = false;
+            s_best = dinf();
         }
         __syncthreads();
         const long long s = sm.sid[0];
@@ -1536,6 +1556,9 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
         }
 
+        // stage times non-decreasing in b and I (non-negative coefficients): the row
+        // optimum is then monotone in the row, which the gamma-level pruning needs
+        const bool mono = c1d >= 0.0 && c2d >= 0.0 && c1v >= 0.0 && c2v >= 0.0 && C.dl >= 0.0;
         // ---- P3: each warp pulls gamma values and runs Algorithm 1
         if (!bad && !bad_alpha) {
             for (;;) {
@@ -1557,7 +1580,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 if constexpr (TILE) {
                     t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
                                              C.rows_stride, dpc, C.gmin + gi, alpha,
-                                             c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active);
+                                             c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active,
+                                             (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
                     // 2, 3, ... in sorted order until the pipelined latency stops improving
@@ -1592,6 +1616,13 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
+                }
+                {   // best finished T_inf so far (gamma-level pruning of the later DPs)
+                    double tv = (lane % GL == 0 && active) ? t : dinf();
+#pragma unroll
+                    for (int o = GL; o < 32; o <<= 1) tv = fmin(tv, __shfl_xor_sync(0xffffffffu, tv, o));
+                    if (lane == 0 && tv < s_best) s_best = tv;
+                    __syncwarp();
                 }
             }
         }
