@@ -170,3 +170,28 @@ def test_actual_output_nopipe(orc):
         ends = [2, 5, 7]
         assert rel(orc.eval_actual(pd, Is, np.full(7, 200, np.int32), a, g, ends),
                    orc.eval_plan_nopipe(pd, Is, a, g, ends)) < 1e-14
+
+
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_row_optimum_monotone_in_prefix(orc, pair):
+    """T*(i), the optimal pipelined latency of the i shortest tasks (Algorithm 1's
+    row value, eq:time), is non-decreasing in i: dropping the longest task from its
+    batch shrinks the batch and cannot raise its padded length, so no stage time
+    grows.  The GPU's gamma-level pruning rests on this; checked
+    here on the oracle, prefix by prefix, with binding memory windows included."""
+    K = 24
+    base = scengen.params(pair, K=K, gamma_min=1, gamma_max=6)
+    J, h1, h2 = scengen.MODELS[pair.split("-")[0]]
+    tight = orc.param_memory(J, h1, h2) + 6 * orc.kv_memory_per_task(J, h1, 256, base["O_max"])
+    sc = scengen.generate(77, K, 0, 6, I_max=1024)
+    for pd in (base, dict(base, mem_capacity_bytes=int(tight))):
+        for s in range(6):
+            Is = np.sort(sc["I"][s])
+            for gamma in (1, 3, 6):
+                prev = 0.0
+                for i in range(1, K + 1):
+                    t = orc.dp(dict(pd, K=i), Is[:i], float(sc["alpha"][s]), gamma)[0]
+                    if not np.isfinite(t):
+                        break
+                    assert t >= prev * (1 - 1e-12), (s, gamma, i, t, prev)
+                    prev = t
