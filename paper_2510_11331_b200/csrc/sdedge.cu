@@ -2019,10 +2019,13 @@ int sdedge_solve_batch(const sdedge_scenarios* s, int64_t n, const sdedge_params
 int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
                             sdedge_schedule* o)
 {
-    // Host buffers in, host buffers out.  The batch is cut into <= 16 chunks that
-    // alternate between two internal streams, so the H2D copy of chunk c+1 and
-    // the D2H copy of chunk c-1 overlap the solve of chunk c; the caller's
-    // stream is joined at the end (one cudaMemcpyAsync per array and chunk).
+    // Host buffers in, host buffers out.  The batch is cut into <= 16 chunks; all
+    // H2D copies go in order on one internal stream, all D2H copies on another,
+    // and the solves alternate between two compute streams, chained by events
+    // (solve c after H2D c, D2H c after solve c).  So both copy directions run
+    // back to back while chunks are solved, and the solves of neighbouring chunks
+    // can overlap each other's tail.  The caller's stream is joined at the end
+    // (one cudaMemcpyAsync per array and chunk).
     g_err[0] = 0;
     g_launches = 0;
     int rc = validate(s, n, p, out_latency, o);
@@ -2042,14 +2045,21 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     CU(cudaGetDevice(&dev));
     if (int rc2 = keep_pool_cached(dev)) return rc2;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&d), off, st));
-    cudaStream_t ss[2] = {nullptr, nullptr};
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-    for (int q = 0; q < 2; ++q) CU(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
-    for (int q = 0; q < 3; ++q) CU(cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming));
-    CU(cudaEventRecord(ev[0], st));
-    for (int q = 0; q < 2; ++q) CU(cudaStreamWaitEvent(ss[q], ev[0], 0));
+    constexpr int kS = 4;                    // 0: H2D, 1-2: solves, 3: D2H
+    constexpr int kMaxCh = 16;
+    cudaStream_t ss[kS] = {};
+    cudaEvent_t ev0 = nullptr, evh[kMaxCh] = {}, evc[kMaxCh] = {}, evj[kS] = {};
+    for (int q = 0; q < kS; ++q) CU(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    for (int q = 0; q < kMaxCh; ++q) {
+        CU(cudaEventCreateWithFlags(&evh[q], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&evc[q], cudaEventDisableTiming));
+    }
+    for (int q = 0; q < kS; ++q) CU(cudaEventCreateWithFlags(&evj[q], cudaEventDisableTiming));
+    CU(cudaEventRecord(ev0, st));
+    for (int q = 0; q < kS; ++q) CU(cudaStreamWaitEvent(ss[q], ev0, 0));
 
-    const long long nch = std::max(1LL, std::min(16LL, (long long)(n / 32768)));
+    const long long nch = std::max(1LL, std::min((long long)kMaxCh, (long long)(n / 32768)));
     const long long chunk = (n + nch - 1) / nch;
     int launches = 0;
     auto h2d = [&](size_t doff, const void* src, size_t row, long long a, long long m, cudaStream_t q) {
@@ -2063,12 +2073,15 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     for (long long c = 0; c < nch; ++c) {
         const long long a = c * chunk, m = std::min(chunk, (long long)n - a);
         if (m <= 0) break;
-        cudaStream_t q = ss[c & 1];
+        cudaStream_t q = ss[0];
         CU(h2d(oI, s->input_len, K * 4, a, m, q));
         CU(h2d(oP, s->tx_power_w, K * 8, a, m, q));
         CU(h2d(oG, s->gain, K * 8, a, m, q));
         CU(h2d(oA, s->alpha, 8, a, m, q));
         if (bC) CU(h2d(oC, s->coeffs, 32, a, m, q));
+        CU(cudaEventRecord(evh[c], q));
+        q = ss[1 + (c & 1)];
+        CU(cudaStreamWaitEvent(q, evh[c], 0));
         sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI) + a * K, reinterpret_cast<double*>(d + oP) + a * K,
                             reinterpret_cast<double*>(d + oG) + a * K, reinterpret_cast<double*>(d + oA) + a,
                             bC ? reinterpret_cast<double*>(d + oC) + a * 4 : nullptr};
@@ -2081,6 +2094,9 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
         rc = solve_device(&ds, m, &pc, reinterpret_cast<double*>(d + oLat) + 3 * a, &dsch);
         if (rc) return rc;
         launches += g_launches;
+        CU(cudaEventRecord(evc[c], q));
+        q = ss[3];
+        CU(cudaStreamWaitEvent(q, evc[c], 0));
         CU(d2h(out_latency, oLat, 24, a, m, q));
         CU(d2h(o->gamma, oGm, 4, a, m, q));
         CU(d2h(o->num_batches, oM, 4, a, m, q));
@@ -2089,13 +2105,18 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
         if (bW) CU(d2h(o->bw_share, oW, K * 8, a, m, q));
         CU(d2h(o->status, oSt, 4, a, m, q));
     }
-    for (int q = 0; q < 2; ++q) {
-        CU(cudaEventRecord(ev[1 + q], ss[q]));
-        CU(cudaStreamWaitEvent(st, ev[1 + q], 0));
+    for (int q = 0; q < kS; ++q) {
+        CU(cudaEventRecord(evj[q], ss[q]));
+        CU(cudaStreamWaitEvent(st, evj[q], 0));
     }
     CU(cudaFreeAsync(d, st));
-    for (int q = 0; q < 2; ++q) CU(cudaStreamDestroy(ss[q]));   // released once their work drains
-    for (int q = 0; q < 3; ++q) CU(cudaEventDestroy(ev[q]));
+    for (int q = 0; q < kS; ++q) CU(cudaStreamDestroy(ss[q]));   // released once their work drains
+    CU(cudaEventDestroy(ev0));
+    for (int q = 0; q < kMaxCh; ++q) {
+        CU(cudaEventDestroy(evh[q]));
+        CU(cudaEventDestroy(evc[q]));
+    }
+    for (int q = 0; q < kS; ++q) CU(cudaEventDestroy(evj[q]));
     g_launches = launches;
     return 0;
 }
