@@ -92,9 +92,27 @@ struct Outputs {
 };
 
 // Work actually evaluated by one lane (reduced per CTA, flushed once at exit).
+// Work counters: accumulated in shared memory at the end of
+// each DP (warp-reduced), not carried in registers across the gamma loop.
+// Slots: candidates, candidate-segments, candidate-steps W, rows, full evaluations.
 struct WorkCount {
-    unsigned long long cand = 0, seg = 0, steps = 0, rows = 0, full = 0;
+    unsigned long long* sh;
 };
+
+__device__ inline void work_flush(const WorkCount& wc, bool active, unsigned cand, unsigned seg, unsigned full,
+                                  unsigned long long steps, unsigned rows)
+{
+    unsigned long long v[5] = {active ? cand : 0u, active ? seg : 0u, active ? steps : 0ull, active ? rows : 0u,
+                               active ? full : 0u};
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) atomicAdd(wc.sh + q, v[q]);
+}
 
 struct Work {
     short* S;                      // [grid][ng][K] boundaries j* (1-based), one block per CTA
@@ -766,13 +784,8 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         T_last = (double)tmin;
     }
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
-    if (active) {
-        wc.cand += n_cand;
-        wc.full += n_cand;
-        wc.seg += n_seg;
-        wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
-        if (gl == 0) wc.rows += rows_done;
-    }
+    work_flush(wc, active, n_cand, n_seg, n_cand, (unsigned long long)n_cand * (unsigned long long)N,
+               gl == 0 ? (unsigned)rows_done : 0u);
     return T_last;
 }
 
@@ -848,6 +861,9 @@ __device__ inline void fence_proxy_async_global()
 #endif
 #ifndef SDEDGE_PASS1_FAST
 #define SDEDGE_PASS1_FAST 1  // phase-A bound test as one FMA + compare per predecessor
+#endif
+#ifndef SDEDGE_SCEN_SMEM
+#define SDEDGE_SCEN_SMEM 1    // re-read alpha and the coefficients from shared memory at each DP call
 #endif
 #ifndef SDEDGE_GAMMA_ABORT
 #define SDEDGE_GAMMA_ABORT 1  // stop a gamma's DP once its partial optimum exceeds the best finished gamma
@@ -1397,13 +1413,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     if (infeasible) T_last = dinf();
     if (aborted) T_last = dinf();            // pruned (or an idle group)
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
-    if (active) {
-        wc.cand += n_cand;
-        wc.seg += n_seg;
-        wc.full += n_full;
-        wc.steps += (unsigned long long)n_cand * (unsigned long long)N;
-        if (gl == 0) wc.rows += rows_done;
-    }
+    work_flush(wc, active, n_cand, n_seg, n_full, (unsigned long long)n_cand * (unsigned long long)N,
+               gl == 0 ? (unsigned)rows_done : 0u);
     return T_last;
 }
 
@@ -1461,7 +1472,9 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     __shared__ unsigned long long s_work[5];
     __shared__ long long s_top[kWarps * G];
     if (tid < 5) s_work[tid] = 0;
-    WorkCount wc;
+    __syncthreads();
+    WorkCount wc{s_work};
+    __shared__ double s_par[5];              // alpha, c1d, c2d, c1v, c2v of the current scenario
 
     for (;;) {
         if (tid == 0) {
@@ -1541,24 +1554,27 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                                  : (short)((e % b == 0 || e == K) ? ((e - 1) / b) * b + 1 : 0);
             }
         }
+        if (tid == 0) {
+            s_par[0] = in.alpha[s];
+            s_par[1] = in.coeffs ? in.coeffs[4 * s] : C.c1d;
+            s_par[2] = in.coeffs ? in.coeffs[4 * s + 1] : C.c2d;
+            s_par[3] = in.coeffs ? in.coeffs[4 * s + 2] : C.c1v;
+            s_par[4] = in.coeffs ? in.coeffs[4 * s + 3] : C.c2v;
+        }
         __syncthreads();
-        double Tcom = 0.0, qsum = 0.0;
-        for (int w = 0; w < kWarps; ++w) {
-            Tcom = uniform ? fmax(Tcom, sm.red[w]) : Tcom + sm.red[w];
-            qsum += sm.red[kWarps + w];
-        }
-
-        const double alpha = in.alpha[s];
-        const bool bad_alpha = !(alpha > 0.0 && alpha < 1.0);
-        double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
-        if (in.coeffs) {
-            c1d = in.coeffs[4 * s]; c2d = in.coeffs[4 * s + 1];
-            c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
-        }
+        const bool bad_alpha = !(s_par[0] > 0.0 && s_par[0] < 1.0);
+        // (alpha and the coefficients are re-read from shared memory at each DP call:
+        // nothing scenario-wide stays live in registers across the gamma loop)
+#if SDEDGE_SCEN_SMEM
+#define SDEDGE_SCEN_ARGS s_par[0], s_par[1], s_par[2], s_par[3], s_par[4]
+#else
+        const double alpha = s_par[0], c1d = s_par[1], c2d = s_par[2], c1v = s_par[3], c2v = s_par[4];
+#define SDEDGE_SCEN_ARGS alpha, c1d, c2d, c1v, c2v
+#endif
 
         // stage times non-decreasing in b and I (non-negative coefficients): the row
         // optimum is then monotone in the row, which the gamma-level pruning needs
-        const bool mono = c1d >= 0.0 && c2d >= 0.0 && c1v >= 0.0 && c2v >= 0.0 && C.dl >= 0.0;
+        const bool mono = s_par[1] >= 0.0 && s_par[2] >= 0.0 && s_par[3] >= 0.0 && s_par[4] >= 0.0 && C.dl >= 0.0;
         // ---- P3: each warp pulls gamma values and runs Algorithm 1
         if (!bad && !bad_alpha) {
             for (;;) {
@@ -1579,8 +1595,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 constexpr bool kBase = G == 1 && !TILE;
                 if constexpr (TILE) {
                     t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
-                                             C.rows_stride, dpc, C.gmin + gi, alpha,
-                                             c1d, c2d, c1v, c2v, Sg, &ovf, wc, &s_top[warp * G + grp], active,
+                                             C.rows_stride, dpc, C.gmin + gi, SDEDGE_SCEN_ARGS,
+                                             Sg, &ovf, wc, &s_top[warp * G + grp], active,
                                              (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
@@ -1597,8 +1613,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     int bb = 1;
                     for (int b = K >= 2 ? 2 : 1; b <= K; ++b) {
                         plan(b);
-                        const double tt = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v,
-                                                               c2v, nullptr, &ovf, wc, &s_top[warp * G + grp],
+                        const double tt = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS,
+                                                               nullptr, &ovf, wc, &s_top[warp * G + grp],
                                                                active, jw);
                         if (!(tt < tb) && !isinf(tb)) break;       // latency starts to degrade
                         if (isinf(tt)) break;                      // memory binds
@@ -1607,10 +1623,10 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     }
                     if (isinf(tb)) bb = 1;
                     plan(bb);
-                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v, Sg, &ovf, wc,
+                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
                                              &s_top[warp * G + grp], active, jw);
                 } else {
-                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, alpha, c1d, c2d, c1v, c2v, Sg, &ovf, wc,
+                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
                                              &s_top[warp * G + grp], active, kBase ? jf : nullptr);
                 }
                 if (lane % GL == 0 && active) {
@@ -1638,6 +1654,11 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             continue;
         }
 
+        double Tcom = 0.0, qsum = 0.0;       // eq:opt_w sums (per-warp partials in sm.red)
+        for (int w = 0; w < kWarps; ++w) {
+            Tcom = uniform ? fmax(Tcom, sm.red[w]) : Tcom + sm.red[w];
+            qsum += sm.red[kWarps + w];
+        }
         // ---- gamma* (smallest argmin, reading A7) and backtrack (reading A5)
         if (tid == 0) {
             int st = 0, gbest = -1, M = 0;
@@ -1679,19 +1700,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             for (int k = tid; k < K; k += kThreads) {
                 double wk = dnan();
                 if (!sm.ctl[3]) {
-                    const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
-                    wk = C.bw_policy == SDEDGE_BW_UNIFORM ? 1.0 / K : ((double)Ig[k] / sk) / qsum;
+                    const double sk = log2(1.0 + in.p[s * K + k] * in.g[s * K + k] / C.sigma2);
+                    wk = C.bw_policy == SDEDGE_BW_UNIFORM ? 1.0 / K : ((double)in.I[s * K + k] / sk) / qsum;
                 }
                 out.w[s * K + k] = wk;
             }
         __syncthreads();
     }
     if (out.work) {
-        unsigned long long v[5] = {wc.cand, wc.seg, wc.steps, wc.rows, wc.full};
-        for (int q = 0; q < 5; ++q) {
-            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
-            if (lane == 0) atomicAdd(&s_work[q], v[q]);
-        }
         __syncthreads();
         if (tid < 5) atomicAdd(out.work + tid, s_work[tid]);
     }
