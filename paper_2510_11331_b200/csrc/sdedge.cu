@@ -1137,6 +1137,25 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     __syncwarp();
     int rows_done = 0;
     bool ovf_any = false, infeasible = false, aborted = !active;
+#if SDEDGE_GAMMA_ABORT
+    if (best_s) {
+        // Before any row: T_inf >= the verify server's total work, sum_m sum_n T^v_n =
+        // sum_m (b_m vsl(I_m) + vc) >= sum_k vsl(I_k) + vc, since vsl grows with I and
+        // each task pays at least its own length's slope.  A gamma whose
+        // bound already exceeds the best finished T_inf never starts.
+        double lbv = 0.0;
+        for (int r = gl; r < K; r += GL) lbv += row_coef(D, sm.Is[r]).vsl;
+#pragma unroll
+        for (int o = 1; o < GL; o <<= 1) lbv += __shfl_xor_sync(0xffffffffu, lbv, o);
+        lbv += D.c2vv * (D.Mx + 1.0);
+        const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;       // covers the rounding of either DP
+        aborted |= lbv * (1.0 - mg) > *best_s * (1.0 + mg);
+        if (__all_sync(0xffffffffu, aborted)) {
+            work_flush(wc, active, 0u, 0u, 0u, 0ull, 0u);
+            return dinf();
+        }
+    }
+#endif
     R t_row = (R)0;                          // Upsilon[i,0,0] of the last row this lane finalized
     int jprev = 0;                           // j* of row i0-1 (the previous tile's last row)
     for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
