@@ -195,3 +195,35 @@ def test_row_optimum_monotone_in_prefix(orc, pair):
                         break
                     assert t >= prev * (1 - 1e-12), (s, gamma, i, t, prev)
                     prev = t
+
+
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_t_inf_at_least_total_verify_work(orc, pair):
+    """T_inf(gamma) >= sum_k vsl(I_k) + vc: every step's pipeline makespan is at
+    least the verify stage's serial work (eq:time), a batch's verify time is affine
+    in its size with a slope that grows with the padded length (eq:flops_v,
+    eq:latency_b2), so each task pays at least its own length's slope and the
+    last batch at least the intercept.  The GPU skips a gamma whose bound exceeds
+    the best finished T_inf; this pins the bound on the oracle's
+    literal DP and stage-time functions."""
+    K = 12
+    pd = scengen.params(pair, K=K, gamma_min=1, gamma_max=8, O_max=256)
+    sc = scengen.generate(91, K, 0, 5)
+    for s in range(5):
+        Is = np.sort(sc["I"][s])
+        alpha = float(sc["alpha"][s])
+        for gamma in (1, 2, 5, 8):
+            L = orc.expected_tokens(alpha, gamma)
+            N = orc.decode_steps(pd["O_max"], L)
+            t_inf = orc.dp(pd, Is, alpha, gamma)[0]
+            lb = 0.0
+            for n in range(1, N + 1):
+                for I in Is:
+                    t1 = orc.verify_time(pd, 1, int(I), gamma, L, n)
+                    t2 = orc.verify_time(pd, 2, int(I), gamma, L, n)
+                    lb += t2 - t1                                # this task's slope at its own length
+                t1 = orc.verify_time(pd, 1, int(Is[-1]), gamma, L, n)
+                t2 = orc.verify_time(pd, 2, int(Is[-1]), gamma, L, n)
+                lb += 2 * t1 - t2                                # one intercept
+            assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
+            assert lb > 0.5 * t_inf or pair != "68M-7B"          # and it is not vacuous for a small draft
