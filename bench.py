@@ -49,10 +49,10 @@ OPS = {"dense": dict(cand=16, seg=0, step=4, row=40, pruned=0),
 
 # DRAM bytes (read + write) per scenario of the envelope kernel from the one
 # `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_final_c4.md:
-# 0.34 GB read + 1.62 GB written for a 1e5-scenario C4 launch), scaled to the
+# 0.29 GB read + 0.91 GB written for a 1e5-scenario C4 launch), scaled to the
 # launch.  The algorithmic bytes are 2568 in + 2084 out per scenario; the rest
 # is the write-back of the tiled DP's global row store.
-NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (0.33715968e9 + 1.61981e9) / 1e5}
+NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (0.29304576e9 + 0.912838656e9) / 1e5}
 
 
 def parse():
