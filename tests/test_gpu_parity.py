@@ -164,6 +164,18 @@ def test_narrow_memory_windows(pair, bmax):
     assert len(ends) > 0 and max(ends) <= 2 * bmax + 2     # the windows really bind
 
 
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-13B"])
+def test_high_acceptance_gamma_pruning(pair):
+    """High acceptance rates (alpha in [0.9, 0.99)) move gamma* away from 1, so the
+    gamma-level pruning works against a best found late and
+    prunes in a different pattern; results must still match the oracle."""
+    pd = scengen.params(pair, K=48, gamma_min=1, gamma_max=12)
+    sc = scengen.generate(55, 48, 0, 200, alpha_lo=0.9, alpha_hi=0.99)
+    res, orc, g = _check(pd, sc, 0, ENV)
+    assert res["failures"] == 0
+    assert len(set(int(x) for x in orc["gamma"])) > 2        # a spread of gamma*, not all 1
+
+
 def test_invalid_scenarios_status():
     pd = scengen.params("68M-7B", K=8, gamma_min=1, gamma_max=3)
     sc = scengen.generate(23, 8, 0, 6)
