@@ -156,6 +156,23 @@ int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const 
 int sdedge_evaluate_actual(const sdedge_scenarios* scenarios, const int32_t* output_len, int64_t n,
                            const sdedge_params* params, const sdedge_schedule* plan, double* out_t_inf);
 
+/* Exhaustive search (quantifies Algorithm 1's heuristic
+ * gap).  For each scenario: the exact minimum of the planned T_inf
+ * (eq:time, eq:latency_inf P:505-530, uniform O_max as P:638-641) over EVERY
+ * contiguous partition of the stably sorted order (the search space of
+ * Algorithm 1), every gamma in [gamma_min, gamma_max] and subject to the memory
+ * constraint (b) per batch.  2^(K-1) plans per gamma, so K must
+ * be <= 20 (-1 otherwise).  batching_policy selects the cost: SDEDGE_BATCH_PROPOSED
+ * (pipelined) or SDEDGE_BATCH_NO_PIPELINE; any other policy returns -1.  Ties keep
+ * the first plan in (gamma ascending, partition mask ascending) order.
+ * DEVICE pointers; async on params->stream.  out_t_inf: [n] (+inf if no plan is
+ * memory-feasible, NaN for status 2/3).  out: gamma, num_batches, batch_end, order,
+ * status as for sdedge_solve_batch (bw_share ignored; p_k, g_k are not read);
+ * work_counters, if set, accumulates [0] plans evaluated, [1] batch-steps
+ * (sum over plans of N_gamma x M).  Returns 0 / -1 / -2. */
+int sdedge_brute_force(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
+                       double* out_t_inf, sdedge_schedule* out);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int sdedge_last_launch_count(void);
 

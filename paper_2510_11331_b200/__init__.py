@@ -12,7 +12,7 @@ import os
 
 from ._build import LIB, build  # noqa: F401
 
-__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual", "evaluate_actual", "sdedge_pipe_peak", "sdedge_last_error",
+__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual", "evaluate_actual", "sdedge_brute_force", "brute_force", "sdedge_pipe_peak", "sdedge_last_error",
            "sdedge_last_launch_count", "sdedge_abi_version", "solve", "solve_host", "make_params",
            "ALGO_ENVELOPE", "ALGO_DENSE", "EXPORTED_SYMBOLS", "lib"]
 
@@ -21,7 +21,8 @@ BW_OPTIMAL, BW_UNIFORM = 0, 1
 BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC = range(6)
 FLAG_TINY_POOL = 1
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
-                    "sdedge_last_launch_count", "sdedge_last_error", "sdedge_abi_version", "sdedge_pipe_peak")
+                    "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
+                    "sdedge_abi_version", "sdedge_pipe_peak")
 
 
 class SdedgeModel(C.Structure):
@@ -70,6 +71,9 @@ def lib() -> C.CDLL:
         L.sdedge_evaluate_actual.restype = C.c_int
         L.sdedge_evaluate_actual.argtypes = [C.POINTER(SdedgeScenarios), C.c_void_p, C.c_int64,
                                              C.POINTER(SdedgeParams), C.POINTER(SdedgeSchedule), C.c_void_p]
+        L.sdedge_brute_force.restype = C.c_int
+        L.sdedge_brute_force.argtypes = [C.POINTER(SdedgeScenarios), C.c_int64, C.POINTER(SdedgeParams),
+                                         C.c_void_p, C.POINTER(SdedgeSchedule)]
         L.sdedge_last_error.restype = C.c_char_p
         L.sdedge_last_launch_count.restype = C.c_int
         L.sdedge_abi_version.restype = C.c_int
@@ -160,6 +164,35 @@ def evaluate_actual(params: dict, I, p, g, alpha, output_len, plan: dict, coeffs
     sdedge_evaluate_actual(I, p, g, alpha, coeffs, output_len, n, P, plan["gamma"], plan["M"], plan["batch_end"],
                            plan["order"], plan["status"], out)
     return out
+
+
+def sdedge_brute_force(I, alpha, coeffs, n, params: SdedgeParams, out_t_inf, gamma, num_batches, batch_end,
+                       order, status, work_counters=None):
+    """Direct C-ABI call (DEVICE tensors): exhaustive search over contiguous plans and gamma (K <= 20)."""
+    sc = SdedgeScenarios(_ptr(I), None, None, _ptr(alpha), _ptr(coeffs))
+    sch = SdedgeSchedule(_ptr(gamma), _ptr(num_batches), _ptr(batch_end), _ptr(order), None, _ptr(status),
+                         _ptr(work_counters))
+    rc = lib().sdedge_brute_force(C.byref(sc), n, C.byref(params), _ptr(out_t_inf), C.byref(sch))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_brute_force failed ({rc}): {sdedge_last_error()}")
+    return rc
+
+
+def brute_force(params: dict, I, alpha, coeffs=None, stream=None, work_counters=None) -> dict:
+    """Exact optimum over every contiguous plan and gamma for CUDA-resident
+    scenarios (K <= 20); returns CUDA tensors t_inf, gamma, M, batch_end, order, status."""
+    import torch
+    n, K = I.shape
+    if stream is None:
+        stream = torch.cuda.current_stream(I.device)
+    P = make_params(dict(params, K=K), stream=stream)
+    kw = dict(device=I.device)
+    o = dict(t_inf=torch.empty(n, dtype=torch.float64, **kw), gamma=torch.empty(n, dtype=torch.int32, **kw),
+             M=torch.empty(n, dtype=torch.int32, **kw), batch_end=torch.empty((n, K), dtype=torch.int32, **kw),
+             order=torch.empty((n, K), dtype=torch.int32, **kw), status=torch.empty(n, dtype=torch.int32, **kw))
+    sdedge_brute_force(I, alpha, coeffs, n, P, o["t_inf"], o["gamma"], o["M"], o["batch_end"], o["order"],
+                       o["status"], work_counters)
+    return o
 
 
 def sdedge_pipe_peak(fp32: bool = False):

@@ -1826,6 +1826,162 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
     }
 }
 
+// ------------------------------------------------------------ exhaustive search
+// Exact optimum of the batching subproblem over every contiguous partition of
+// the sorted order (the search space of Algorithm 1) and every gamma,
+// to measure Algorithm 1's heuristic gap at scale.  One CTA per
+// scenario (grid-stride); per gamma the per-end-position stage coefficients go
+// to shared memory, each warp takes partitions (bit t of the mask = a batch
+// ends at sorted position t + 1), and its lanes take decoding steps n and run
+// the eq:time recursion over the batches, as in actual_kernel.  Ties keep the
+// first plan in (gamma, mask) order (the oracle's exhaustive search does the same).
+constexpr int kBFMaxK = 20;
+constexpr int kBFWarps = 8;
+
+__global__ void __launch_bounds__(kBFWarps * 32)
+brute_force_kernel(const Consts C, const Inputs in, long long n, double* __restrict__ out_t,
+                   int32_t* __restrict__ og, int32_t* __restrict__ oM, int32_t* __restrict__ obend,
+                   int32_t* __restrict__ oorder, int32_t* __restrict__ ostatus, unsigned long long* work)
+{
+    __shared__ int Is[kBFMaxK], ord[kBFMaxK], bmx[kBFMaxK];
+    __shared__ RowCoef rcs[kBFMaxK];
+    __shared__ double wv[kBFWarps];
+    __shared__ int wg[kBFWarps];
+    __shared__ unsigned wm[kBFWarps];
+    const int K = C.K, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned nmask = 1u << (K - 1), last = 1u << (K - 1);
+    const bool nopipe = C.batch_policy == SDEDGE_BATCH_NO_PIPELINE;
+    unsigned long long plans = 0, bsteps = 0;
+    for (long long s = blockIdx.x; s < n; s += gridDim.x) {
+        int bad = 0;
+        for (int k = tid; k < K; k += blockDim.x) {
+            const int Ik = in.I[s * K + k];
+            bad |= Ik < 1;
+            int r = 0;                                   // stable rank
+            for (int q = 0; q < K; ++q) {
+                const int Iq = in.I[s * K + q];
+                r += (Iq < Ik) || (Iq == Ik && q < k);
+            }
+            ord[r] = k;
+            Is[r] = Ik;
+        }
+        bad = __syncthreads_or(bad);
+        const double alpha = in.alpha[s];
+        const int st0 = bad ? 3 : (!(alpha > 0.0 && alpha < 1.0) ? 2 : 0);
+        for (int r = tid; r < K; r += blockDim.x) {      // memory window
+            const long long room = C.gamma_s - C.Gp;
+            const long long b = room >= 0 ? room / (C.kvunit * ((long long)Is[r] + C.O_max)) : 0;
+            bmx[r] = (int)(b < K ? b : K);
+        }
+        double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
+        if (in.coeffs) {
+            c1d = in.coeffs[4 * s]; c2d = in.coeffs[4 * s + 1];
+            c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
+        }
+        double best = kinf<double>();
+        int bg = -1;
+        unsigned bm = 0;
+        for (int gi = 0; st0 == 0 && gi < C.ng; ++gi) {
+            const int g = C.gmin + gi;
+            const double L = expected_tokens(alpha, g);
+            const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n, O = O_max
+            DPConst D;
+            D.g = g;
+            D.tri = D.g * (D.g - 1.0) * 0.5;
+            D.kd = c1d * (4.0 * C.Jd * (double)C.hd);
+            D.kv = c1v * (4.0 * C.Jv * (double)C.hv);
+            D.hd2 = 2.0 * C.hd + C.h2d;
+            D.hv2 = 2.0 * C.hv + C.h2v;
+            D.bdc = D.kd * D.g * L;
+            D.bvc = D.kv * (1.0 + D.g) * L;
+            D.c2dg = D.g * c2d;
+            D.c2vv = c2v + C.dl;
+            D.Mx = 0.0;
+            D.sumM = 0.0;
+            __syncthreads();                             // previous gamma's readers are done
+            for (int r = tid; r < K; r += blockDim.x) rcs[r] = row_coef(D, Is[r]);
+            __syncthreads();
+            for (unsigned mask = warp; mask < nmask; mask += kBFWarps) {
+                const unsigned ends = mask | last;
+                bool ok = true;
+                int M = 0;
+                for (unsigned m = ends, st = 1; m; m &= m - 1) {   // cons. (b) per batch
+                    const int e = __ffs(m);
+                    ok &= (e - (int)st + 1) <= bmx[e - 1];
+                    st = e + 1;
+                    ++M;
+                }
+                if (!ok) continue;
+                double acc = 0.0;
+                for (int step = 1 + lane; step <= N; step += 32) {
+                    const double x = step - 1;
+                    double Cd = 0.0, Cc = 0.0;
+                    for (unsigned m = ends, st = 1; m; m &= m - 1) {
+                        const int e = __ffs(m);
+                        const double b = e - (int)st + 1;
+                        st = e + 1;
+                        const RowCoef& r = rcs[e - 1];   // padded to the batch's longest input
+                        const double td = step == 1 ? fma(b, r.td1, D.c2dg) : fma(b * D.bdc, x, fma(b, r.ad, D.c2dg));
+                        const double tv = step == 1 ? fma(b, r.tv1, D.c2vv) : fma(b * D.bvc, x, fma(b, r.av, D.c2vv));
+                        if (nopipe) { Cc += td + tv; continue; }
+                        Cd += td;                        // C^d_{n,m}
+                        Cc = rmax(Cd, Cc) + tv;          // eq:time
+                    }
+                    acc += Cc;                           // T_n = C_{n,M}
+                }
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                acc = __shfl_sync(0xffffffffu, acc, 0);  // warp-uniform decision
+                ++plans;
+                bsteps += (unsigned long long)N * M;
+                if (acc < best) { best = acc; bg = g; bm = mask; }
+            }
+        }
+        if (lane == 0) { wv[warp] = best; wg[warp] = bg; wm[warp] = bm; }
+        __syncthreads();
+        if (warp == 0) {
+            double v = kinf<double>();
+            int g = -1;
+            unsigned mk = 0;
+            for (int w = 0; w < kBFWarps; ++w) {
+                if (wg[w] < 0) continue;
+                if (g < 0 || wv[w] < v || (wv[w] == v && (wg[w] < g || (wg[w] == g && wm[w] < mk)))) {
+                    v = wv[w]; g = wg[w]; mk = wm[w];
+                }
+            }
+            const int st = st0 ? st0 : (g < 0 ? 1 : 0);
+            const unsigned ends = mk | last;
+            const int M = st ? 0 : __popc(ends);
+            for (int q = lane; q < K; q += 32) {
+                int32_t be = 0;
+                if (st == 0 && q < M) {                  // position of the (q+1)-th set bit
+                    unsigned m = ends;
+                    for (int t = 0; t < q; ++t) m &= m - 1;
+                    be = __ffs(m);
+                }
+                obend[s * K + q] = be;
+                oorder[s * K + q] = ord[q];
+            }
+            if (lane == 0) {
+                out_t[s] = st == 0 ? v : (st == 1 ? kinf<double>() : dnan());
+                og[s] = st ? -1 : g;
+                oM[s] = M;
+                ostatus[s] = st;
+            }
+        }
+        __syncthreads();
+    }
+    if (work) {
+        for (int o = 16; o > 0; o >>= 1) {
+            plans += __shfl_xor_sync(0xffffffffu, plans, o);
+            bsteps += __shfl_xor_sync(0xffffffffu, bsteps, o);
+        }
+        if (lane == 0) {          // plans/bsteps are per warp (lane-uniform): count once per warp
+            atomicAdd(work + 0, plans / 32);
+            atomicAdd(work + 1, bsteps / 32);
+        }
+    }
+}
+
 // ------------------------------------------------------------ pipe-peak microbenchmark
 template <typename T>
 __global__ void pipe_peak_kernel(T* sink, int iters, T seed)
@@ -2185,6 +2341,37 @@ int sdedge_evaluate_actual(const sdedge_scenarios* s, const int32_t* output_len,
     actual_kernel<<<(unsigned)blocks, warps * 32, sb, st>>>(C, in, output_len, plan->gamma, plan->num_batches,
                                                            plan->batch_end, plan->order, plan->status, n,
                                                            out_t_inf);
+    CU(cudaGetLastError());
+    g_launches = 1;
+    return 0;
+}
+
+int sdedge_brute_force(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_t_inf,
+                       sdedge_schedule* out)
+{
+    g_err[0] = 0;
+    g_launches = 0;
+    sdedge_schedule dummy{};
+    int rc = validate(s, 0, p, nullptr, &dummy);
+    if (rc) return rc;
+    if (n < 0) return fail(-1, "n < 0");
+    if (p->K > kBFMaxK) return fail(-1, "brute force needs K <= 20");
+    if (p->batching_policy != SDEDGE_BATCH_PROPOSED && p->batching_policy != SDEDGE_BATCH_NO_PIPELINE)
+        return fail(-1, "brute force evaluates the pipelined or the no-pipeline cost only");
+    if (n == 0) return 0;
+    if (!s->input_len || !s->alpha || !out || !out_t_inf || !out->gamma || !out->num_batches ||
+        !out->batch_end || !out->order || !out->status)
+        return fail(-1, "null argument");
+    Consts C = make_consts(p);
+    Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
+    int dev = 0, nsm = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const long long blocks = std::min<long long>(n, (long long)nsm * 8);
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    brute_force_kernel<<<(unsigned)blocks, kBFWarps * 32, 0, st>>>(
+        C, in, n, out_t_inf, out->gamma, out->num_batches, out->batch_end, out->order, out->status,
+        reinterpret_cast<unsigned long long*>(out->work_counters));
     CU(cudaGetLastError());
     g_launches = 1;
     return 0;
