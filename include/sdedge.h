@@ -169,7 +169,9 @@ int sdedge_evaluate_actual(const sdedge_scenarios* scenarios, const int32_t* out
  * memory-feasible, NaN for status 2/3).  out: gamma, num_batches, batch_end, order,
  * status as for sdedge_solve_batch (bw_share ignored; p_k, g_k are not read);
  * work_counters, if set, accumulates [0] plans evaluated, [1] batch-steps
- * (sum over plans of N_gamma x M).  Returns 0 / -1 / -2. */
+ * (sum over plans of N_gamma x M).  Two launches: one CTA per (scenario, gamma)
+ * item, then one warp per scenario for the min over gamma; the [n * ngamma]
+ * workspace is stream-ordered.  Returns 0 / -1 / -2 / -3. */
 int sdedge_brute_force(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
                        double* out_t_inf, sdedge_schedule* out);
 

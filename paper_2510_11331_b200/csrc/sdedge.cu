@@ -1829,49 +1829,53 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
 // ------------------------------------------------------------ exhaustive search
 // Exact optimum of the batching subproblem over every contiguous partition of
 // the sorted order (the search space of Algorithm 1) and every gamma,
-// to measure Algorithm 1's heuristic gap at scale.  One CTA per
-// scenario (grid-stride); per gamma the per-end-position stage coefficients go
-// to shared memory, each warp takes partitions (bit t of the mask = a batch
-// ends at sorted position t + 1), and its lanes take decoding steps n and run
-// the eq:time recursion over the batches, as in actual_kernel.  Ties keep the
+// to measure Algorithm 1's heuristic gap at scale.
+// bf_item_kernel: one CTA per (scenario, gamma chunk) item (grid-stride); the chunk
+// is one gamma when n is too small to fill one wave of CTAs (the grid then
+// balances even at a few hundred scenarios), else all of them; the per-end-position stage coefficients
+// go to shared memory, each warp takes partitions (bit t of the mask = a batch
+// ends at sorted position t + 1), and its lanes take decoding steps n and run the
+// eq:time recursion over the batches, as in actual_kernel.  The item's minimum
+// and its first minimising mask go to a workspace; bf_final_kernel (one warp per
+// scenario) takes the smallest gamma among the minima.  Ties therefore keep the
 // first plan in (gamma, mask) order (the oracle's exhaustive search does the same).
 constexpr int kBFMaxK = 20;
 constexpr int kBFWarps = 8;
 
 __global__ void __launch_bounds__(kBFWarps * 32)
-brute_force_kernel(const Consts C, const Inputs in, long long n, double* __restrict__ out_t,
-                   int32_t* __restrict__ og, int32_t* __restrict__ oM, int32_t* __restrict__ obend,
-                   int32_t* __restrict__ oorder, int32_t* __restrict__ ostatus, unsigned long long* work)
+bf_item_kernel(const Consts C, const Inputs in, long long items, int gc, double* __restrict__ wsv,
+               int32_t* __restrict__ wsg, unsigned* __restrict__ wsm, unsigned long long* work)
 {
-    __shared__ int Is[kBFMaxK], ord[kBFMaxK], bmx[kBFMaxK];
+    __shared__ int Is[kBFMaxK], bmx[kBFMaxK];
     __shared__ RowCoef rcs[kBFMaxK];
     __shared__ double wv[kBFWarps];
-    __shared__ int wg[kBFWarps];
     __shared__ unsigned wm[kBFWarps];
+    __shared__ int wgs[kBFWarps];
     const int K = C.K, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nmask = 1u << (K - 1), last = 1u << (K - 1);
     const bool nopipe = C.batch_policy == SDEDGE_BATCH_NO_PIPELINE;
     unsigned long long plans = 0, bsteps = 0;
-    for (long long s = blockIdx.x; s < n; s += gridDim.x) {
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        const int nch = (C.ng + gc - 1) / gc;            // gamma chunks per scenario
+        const long long s = it / nch;
+        const int g0 = C.gmin + (int)(it - s * nch) * gc, g1 = min(g0 + gc, C.gmin + C.ng);
+        __syncthreads();                                 // previous item's readers are done
         int bad = 0;
-        for (int k = tid; k < K; k += blockDim.x) {
+        for (int k = tid; k < K; k += blockDim.x) {      // stable rank sort
             const int Ik = in.I[s * K + k];
             bad |= Ik < 1;
-            int r = 0;                                   // stable rank
+            int r = 0;
             for (int q = 0; q < K; ++q) {
                 const int Iq = in.I[s * K + q];
                 r += (Iq < Ik) || (Iq == Ik && q < k);
             }
-            ord[r] = k;
             Is[r] = Ik;
         }
         bad = __syncthreads_or(bad);
         const double alpha = in.alpha[s];
-        const int st0 = bad ? 3 : (!(alpha > 0.0 && alpha < 1.0) ? 2 : 0);
-        for (int r = tid; r < K; r += blockDim.x) {      // memory window
-            const long long room = C.gamma_s - C.Gp;
-            const long long b = room >= 0 ? room / (C.kvunit * ((long long)Is[r] + C.O_max)) : 0;
-            bmx[r] = (int)(b < K ? b : K);
+        if (bad || !(alpha > 0.0 && alpha < 1.0)) {      // status 3 / 2: set by bf_final_kernel
+            if (tid == 0) { wsv[it] = kinf<double>(); wsg[it] = -1; wsm[it] = 0xffffffffu; }
+            continue;
         }
         double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
         if (in.coeffs) {
@@ -1880,9 +1884,8 @@ brute_force_kernel(const Consts C, const Inputs in, long long n, double* __restr
         }
         double best = kinf<double>();
         int bg = -1;
-        unsigned bm = 0;
-        for (int gi = 0; st0 == 0 && gi < C.ng; ++gi) {
-            const int g = C.gmin + gi;
+        unsigned bm = 0xffffffffu;
+        for (int g = g0; g < g1; ++g) {
             const double L = expected_tokens(alpha, g);
             const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n, O = O_max
             DPConst D;
@@ -1898,14 +1901,19 @@ brute_force_kernel(const Consts C, const Inputs in, long long n, double* __restr
             D.c2vv = c2v + C.dl;
             D.Mx = 0.0;
             D.sumM = 0.0;
-            __syncthreads();                             // previous gamma's readers are done
-            for (int r = tid; r < K; r += blockDim.x) rcs[r] = row_coef(D, Is[r]);
+            __syncthreads();                                 // previous gamma's readers are done
+            for (int r = tid; r < K; r += blockDim.x) {
+                const long long room = C.gamma_s - C.Gp;    // memory window
+                const long long b = room >= 0 ? room / (C.kvunit * ((long long)Is[r] + C.O_max)) : 0;
+                bmx[r] = (int)(b < K ? b : K);
+                rcs[r] = row_coef(D, Is[r]);
+            }
             __syncthreads();
             for (unsigned mask = warp; mask < nmask; mask += kBFWarps) {
                 const unsigned ends = mask | last;
                 bool ok = true;
                 int M = 0;
-                for (unsigned m = ends, st = 1; m; m &= m - 1) {   // cons. (b) per batch
+                for (unsigned m = ends, st = 1; m; m &= m - 1) {   // constraint (b) per batch
                     const int e = __ffs(m);
                     ok &= (e - (int)st + 1) <= bmx[e - 1];
                     st = e + 1;
@@ -1920,64 +1928,98 @@ brute_force_kernel(const Consts C, const Inputs in, long long n, double* __restr
                         const int e = __ffs(m);
                         const double b = e - (int)st + 1;
                         st = e + 1;
-                        const RowCoef& r = rcs[e - 1];   // padded to the batch's longest input
+                        const RowCoef& r = rcs[e - 1];       // padded to the batch's longest input
                         const double td = step == 1 ? fma(b, r.td1, D.c2dg) : fma(b * D.bdc, x, fma(b, r.ad, D.c2dg));
                         const double tv = step == 1 ? fma(b, r.tv1, D.c2vv) : fma(b * D.bvc, x, fma(b, r.av, D.c2vv));
                         if (nopipe) { Cc += td + tv; continue; }
-                        Cd += td;                        // C^d_{n,m}
-                        Cc = rmax(Cd, Cc) + tv;          // eq:time
+                        Cd += td;                            // C^d_{n,m}
+                        Cc = rmax(Cd, Cc) + tv;              // eq:time
                     }
-                    acc += Cc;                           // T_n = C_{n,M}
+                    acc += Cc;                               // T_n = C_{n,M}
                 }
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                acc = __shfl_sync(0xffffffffu, acc, 0);  // warp-uniform decision
+                acc = __shfl_sync(0xffffffffu, acc, 0);      // warp-uniform decision
                 ++plans;
                 bsteps += (unsigned long long)N * M;
-                if (acc < best) { best = acc; bg = g; bm = mask; }
+                if (acc < best) { best = acc; bg = g; bm = mask; }   // (gamma, mask) ascend within a warp
             }
         }
-        if (lane == 0) { wv[warp] = best; wg[warp] = bg; wm[warp] = bm; }
+        if (lane == 0) { wv[warp] = best; wgs[warp] = bg; wm[warp] = bm; }
         __syncthreads();
-        if (warp == 0) {
+        if (tid == 0) {
             double v = kinf<double>();
-            int g = -1;
-            unsigned mk = 0;
-            for (int w = 0; w < kBFWarps; ++w) {
-                if (wg[w] < 0) continue;
-                if (g < 0 || wv[w] < v || (wv[w] == v && (wg[w] < g || (wg[w] == g && wm[w] < mk)))) {
-                    v = wv[w]; g = wg[w]; mk = wm[w];
+            int gb = -1;
+            unsigned mk = 0xffffffffu;
+            for (int w = 0; w < kBFWarps; ++w)          // lexicographic (T_inf, gamma, mask)
+                if (wgs[w] >= 0 && (gb < 0 || wv[w] < v ||
+                                    (wv[w] == v && (wgs[w] < gb || (wgs[w] == gb && wm[w] < mk))))) {
+                    v = wv[w];
+                    gb = wgs[w];
+                    mk = wm[w];
                 }
-            }
-            const int st = st0 ? st0 : (g < 0 ? 1 : 0);
-            const unsigned ends = mk | last;
-            const int M = st ? 0 : __popc(ends);
-            for (int q = lane; q < K; q += 32) {
-                int32_t be = 0;
-                if (st == 0 && q < M) {                  // position of the (q+1)-th set bit
-                    unsigned m = ends;
-                    for (int t = 0; t < q; ++t) m &= m - 1;
-                    be = __ffs(m);
-                }
-                obend[s * K + q] = be;
-                oorder[s * K + q] = ord[q];
-            }
-            if (lane == 0) {
-                out_t[s] = st == 0 ? v : (st == 1 ? kinf<double>() : dnan());
-                og[s] = st ? -1 : g;
-                oM[s] = M;
-                ostatus[s] = st;
-            }
+            wsv[it] = v;
+            wsg[it] = gb;
+            wsm[it] = mk;
         }
-        __syncthreads();
     }
     if (work) {
         for (int o = 16; o > 0; o >>= 1) {
             plans += __shfl_xor_sync(0xffffffffu, plans, o);
             bsteps += __shfl_xor_sync(0xffffffffu, bsteps, o);
         }
-        if (lane == 0) {          // plans/bsteps are per warp (lane-uniform): count once per warp
+        if (lane == 0) {          // plans/bsteps are lane-uniform: count once per warp
             atomicAdd(work + 0, plans / 32);
             atomicAdd(work + 1, bsteps / 32);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128)
+bf_final_kernel(const Consts C, const Inputs in, long long n, int nch, const double* __restrict__ wsv,
+                const int32_t* __restrict__ wsg, const unsigned* __restrict__ wsm, double* __restrict__ out_t, int32_t* __restrict__ og,
+                int32_t* __restrict__ oM, int32_t* __restrict__ obend, int32_t* __restrict__ oorder,
+                int32_t* __restrict__ ostatus)
+{
+    const int K = C.K, lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < n; s += nw) {
+        int rank = 0, bad = 0;
+        if (lane < K) {                                  // stable rank of task `lane`
+            const int Ik = in.I[s * K + lane];
+            bad = Ik < 1;
+            for (int q = 0; q < K; ++q) {
+                const int Iq = in.I[s * K + q];
+                rank += (Iq < Ik) || (Iq == Ik && q < lane);
+            }
+        }
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        const double alpha = in.alpha[s];
+        double v = kinf<double>();
+        int g = -1;
+        unsigned mk = 0;
+        for (int c = 0; c < nch; ++c) {                  // smallest gamma among equal minima
+            const double x = wsv[s * nch + c];
+            const int gc = wsg[s * nch + c];
+            if (gc >= 0 && (g < 0 || x < v)) { v = x; g = gc; mk = wsm[s * nch + c]; }
+        }
+        const int st = bad ? 3 : (!(alpha > 0.0 && alpha < 1.0) ? 2 : (g < 0 ? 1 : 0));
+        const unsigned ends = mk | (1u << (K - 1));
+        const int M = st ? 0 : __popc(ends);
+        if (lane < K) {
+            oorder[s * K + rank] = lane;
+            int32_t be = 0;
+            if (st == 0 && lane < M) {                   // position of the (lane+1)-th set bit
+                unsigned m = ends;
+                for (int t = 0; t < lane; ++t) m &= m - 1;
+                be = __ffs(m);
+            }
+            obend[s * K + lane] = be;
+        }
+        if (lane == 0) {
+            out_t[s] = st == 0 ? v : (st == 1 ? kinf<double>() : dnan());
+            og[s] = st ? -1 : g;
+            oM[s] = M;
+            ostatus[s] = st;
         }
     }
 }
@@ -2367,13 +2409,29 @@ int sdedge_brute_force(const sdedge_scenarios* s, int64_t n, const sdedge_params
     int dev = 0, nsm = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const long long blocks = std::min<long long>(n, (long long)nsm * 8);
+    // gamma chunk per CTA item: all gammas of a scenario in one CTA when there are
+    // enough scenarios to fill a wave of resident CTAs, else one gamma per item
+    const int gc = n >= (long long)nsm * 8 ? C.ng : 1;
+    const int nch = (C.ng + gc - 1) / gc;
+    const long long items = n * (long long)nch;
+    const long long blocks = std::min<long long>(items, (long long)nsm * 8);
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
-    brute_force_kernel<<<(unsigned)blocks, kBFWarps * 32, 0, st>>>(
-        C, in, n, out_t_inf, out->gamma, out->num_batches, out->batch_end, out->order, out->status,
-        reinterpret_cast<unsigned long long*>(out->work_counters));
+    unsigned char* ws = nullptr;
+    const size_t offg = ((size_t)items * sizeof(double) + 255) & ~(size_t)255;
+    const size_t offm = offg + (((size_t)items * sizeof(int32_t) + 255) & ~(size_t)255);
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), offm + (size_t)items * sizeof(unsigned), st));
+    double* wsv = reinterpret_cast<double*>(ws);
+    int32_t* wsg = reinterpret_cast<int32_t*>(ws + offg);
+    unsigned* wsm = reinterpret_cast<unsigned*>(ws + offm);
+    bf_item_kernel<<<(unsigned)blocks, kBFWarps * 32, 0, st>>>(
+        C, in, items, gc, wsv, wsg, wsm, reinterpret_cast<unsigned long long*>(out->work_counters));
     CU(cudaGetLastError());
-    g_launches = 1;
+    const long long fb = std::min<long long>((n + 3) / 4, (long long)nsm * 16);
+    bf_final_kernel<<<(unsigned)fb, 128, 0, st>>>(C, in, n, nch, wsv, wsg, wsm, out_t_inf, out->gamma, out->num_batches,
+                                                  out->batch_end, out->order, out->status);
+    CU(cudaGetLastError());
+    CU(cudaFreeAsync(ws, st));
+    g_launches = 2;
     return 0;
 }
 

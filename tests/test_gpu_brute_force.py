@@ -164,3 +164,21 @@ def test_bf_work_counters():
     steps = sum(oracle.decode_steps(pd["O_max"], oracle.expected_tokens(float(a), gm))
                 for a in sc["alpha"] for gm in range(gmin, gmax + 1))
     assert w[1] == steps * sumM
+
+
+def test_bf_gamma_chunked_launch():
+    """With enough scenarios one CTA takes all gammas of a scenario (the chunked
+    launch); a small call takes one gamma per CTA.  Same arithmetic, so the two
+    launches agree bit for bit; a sample is checked against the oracle."""
+    K, n = 6, 5000
+    pd = scengen.params("1.1B-13B", K=K, gamma_min=1, gamma_max=5)
+    sc = scengen.generate(18, K, 0, n)
+    big = _gpu_bf(pd, sc)
+    sub = {k: (v[:100] if v is not None else None) for k, v in sc.items()}
+    small = _gpu_bf(pd, sub)
+    for k in ("t_inf", "gamma", "M", "batch_end", "order", "status"):
+        assert (big[k][:100] == small[k]).all(), k
+    sub = {k: (v[n - 60:] if v is not None else None) for k, v in sc.items()}
+    g, _ = _check_against_oracle(pd, sub)
+    for k in ("t_inf", "gamma", "M", "batch_end", "order", "status"):
+        assert (big[k][n - 60:] == g[k]).all(), k
