@@ -1833,8 +1833,8 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
 // bf_item_kernel: one CTA per (scenario, gamma chunk) item (grid-stride); the chunk
 // is one gamma when n is too small to fill one wave of CTAs (the grid then
 // balances even at a few hundred scenarios), else all of them; the per-end-position stage coefficients
-// go to shared memory, each warp takes partitions (bit t of the mask = a batch
-// ends at sorted position t + 1), and its lanes take decoding steps n and run the
+// (every gamma of the chunk at once) go to shared memory, each warp takes
+// (gamma, partition) pairs (bit t of the mask = a batch ends at sorted position t + 1), and its lanes take decoding steps n and run the
 // eq:time recursion over the batches, as in actual_kernel.  The item's minimum
 // and its first minimising mask go to a workspace; bf_final_kernel (one warp per
 // scenario) takes the smallest gamma among the minima.  Ties therefore keep the
@@ -1842,23 +1842,29 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
 constexpr int kBFMaxK = 20;
 constexpr int kBFWarps = 8;
 
-__global__ void __launch_bounds__(kBFWarps * 32)
+constexpr int kBFMaxG = 65;     // gamma_max - gamma_min + 1 <= 65 (gamma in 0..64)
+
+struct BFCoef { double td1, ad, tv1, av; };       // row_coef's stage terms (x b, + c2)
+struct BFGam { double bdc, bvc, c2dg, c2vv; int N, pad; };
+
+__global__ void __launch_bounds__(kBFWarps * 32, 4)
 bf_item_kernel(const Consts C, const Inputs in, long long items, int gc, double* __restrict__ wsv,
                int32_t* __restrict__ wsg, unsigned* __restrict__ wsm, unsigned long long* work)
 {
     __shared__ int Is[kBFMaxK], bmx[kBFMaxK];
-    __shared__ RowCoef rcs[kBFMaxK];
+    __shared__ BFCoef rcs[kBFMaxG * kBFMaxK];       // [gamma of the chunk][sorted end position]
+    __shared__ BFGam gms[kBFMaxG];
     __shared__ double wv[kBFWarps];
     __shared__ unsigned wm[kBFWarps];
     __shared__ int wgs[kBFWarps];
     const int K = C.K, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nmask = 1u << (K - 1), last = 1u << (K - 1);
     const bool nopipe = C.batch_policy == SDEDGE_BATCH_NO_PIPELINE;
+    const int nch = (C.ng + gc - 1) / gc;                // gamma chunks per scenario
     unsigned long long plans = 0, bsteps = 0;
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int nch = (C.ng + gc - 1) / gc;            // gamma chunks per scenario
         const long long s = it / nch;
-        const int g0 = C.gmin + (int)(it - s * nch) * gc, g1 = min(g0 + gc, C.gmin + C.ng);
+        const int g0 = C.gmin + (int)(it - s * nch) * gc, gn = min(gc, C.gmin + C.ng - g0);
         __syncthreads();                                 // previous item's readers are done
         int bad = 0;
         for (int k = tid; k < K; k += blockDim.x) {      // stable rank sort
@@ -1882,12 +1888,18 @@ bf_item_kernel(const Consts C, const Inputs in, long long items, int gc, double*
             c1d = in.coeffs[4 * s]; c2d = in.coeffs[4 * s + 1];
             c1v = in.coeffs[4 * s + 2]; c2v = in.coeffs[4 * s + 3];
         }
-        double best = kinf<double>();
-        int bg = -1;
-        unsigned bm = 0xffffffffu;
-        for (int g = g0; g < g1; ++g) {
+        // stage coefficients of every gamma of the chunk at once, so warps run through
+        // (gamma, mask) pairs without a barrier per gamma
+        for (int q = tid; q < gn * K + K; q += blockDim.x) {
+            if (q >= gn * K) {                           // memory window
+                const int r = q - gn * K;
+                const long long room = C.gamma_s - C.Gp;
+                const long long b = room >= 0 ? room / (C.kvunit * ((long long)Is[r] + C.O_max)) : 0;
+                bmx[r] = (int)(b < K ? b : K);
+                continue;
+            }
+            const int gi = q / K, r = q - gi * K, g = g0 + gi;
             const double L = expected_tokens(alpha, g);
-            const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n, O = O_max
             DPConst D;
             D.g = g;
             D.tri = D.g * (D.g - 1.0) * 0.5;
@@ -1901,48 +1913,54 @@ bf_item_kernel(const Consts C, const Inputs in, long long items, int gc, double*
             D.c2vv = c2v + C.dl;
             D.Mx = 0.0;
             D.sumM = 0.0;
-            __syncthreads();                                 // previous gamma's readers are done
-            for (int r = tid; r < K; r += blockDim.x) {
-                const long long room = C.gamma_s - C.Gp;    // memory window
-                const long long b = room >= 0 ? room / (C.kvunit * ((long long)Is[r] + C.O_max)) : 0;
-                bmx[r] = (int)(b < K ? b : K);
-                rcs[r] = row_coef(D, Is[r]);
+            const RowCoef rc = row_coef(D, Is[r]);
+            rcs[gi * K + r] = BFCoef{rc.td1, rc.ad, rc.tv1, rc.av};
+            if (r == 0)
+                gms[gi] = BFGam{D.bdc, D.bvc, D.c2dg, D.c2vv,
+                                (int)ceil(__ddiv_rn((double)C.O_max, L)), 0};   // eq:step_n, O = O_max
+        }
+        __syncthreads();
+        double best = kinf<double>();
+        int bg = -1;
+        unsigned bm = 0xffffffffu;
+        const unsigned total = (unsigned)gn * nmask;
+        for (unsigned w = warp; w < total; w += kBFWarps) {   // (gamma, mask) ascending per warp
+            const int gi = (int)(w >> (K - 1));
+            const unsigned mask = w & (nmask - 1);
+            const unsigned ends = mask | last;
+            bool ok = true;
+            int M = 0;
+            for (unsigned m = ends, st = 1; m; m &= m - 1) {   // constraint (b) per batch
+                const int e = __ffs(m);
+                ok &= (e - (int)st + 1) <= bmx[e - 1];
+                st = e + 1;
+                ++M;
             }
-            __syncthreads();
-            for (unsigned mask = warp; mask < nmask; mask += kBFWarps) {
-                const unsigned ends = mask | last;
-                bool ok = true;
-                int M = 0;
-                for (unsigned m = ends, st = 1; m; m &= m - 1) {   // constraint (b) per batch
+            if (!ok) continue;
+            const BFGam G = gms[gi];
+            const BFCoef* rg = rcs + gi * K;
+            double acc = 0.0;
+            for (int step = 1 + lane; step <= G.N; step += 32) {
+                const double x = step - 1;
+                double Cd = 0.0, Cc = 0.0;
+                for (unsigned m = ends, st = 1; m; m &= m - 1) {
                     const int e = __ffs(m);
-                    ok &= (e - (int)st + 1) <= bmx[e - 1];
+                    const double b = e - (int)st + 1;
                     st = e + 1;
-                    ++M;
+                    const BFCoef r = rg[e - 1];          // padded to the batch's longest input
+                    const double td = step == 1 ? fma(b, r.td1, G.c2dg) : fma(b * G.bdc, x, fma(b, r.ad, G.c2dg));
+                    const double tv = step == 1 ? fma(b, r.tv1, G.c2vv) : fma(b * G.bvc, x, fma(b, r.av, G.c2vv));
+                    if (nopipe) { Cc += td + tv; continue; }
+                    Cd += td;                            // C^d_{n,m}
+                    Cc = rmax(Cd, Cc) + tv;              // eq:time
                 }
-                if (!ok) continue;
-                double acc = 0.0;
-                for (int step = 1 + lane; step <= N; step += 32) {
-                    const double x = step - 1;
-                    double Cd = 0.0, Cc = 0.0;
-                    for (unsigned m = ends, st = 1; m; m &= m - 1) {
-                        const int e = __ffs(m);
-                        const double b = e - (int)st + 1;
-                        st = e + 1;
-                        const RowCoef& r = rcs[e - 1];       // padded to the batch's longest input
-                        const double td = step == 1 ? fma(b, r.td1, D.c2dg) : fma(b * D.bdc, x, fma(b, r.ad, D.c2dg));
-                        const double tv = step == 1 ? fma(b, r.tv1, D.c2vv) : fma(b * D.bvc, x, fma(b, r.av, D.c2vv));
-                        if (nopipe) { Cc += td + tv; continue; }
-                        Cd += td;                            // C^d_{n,m}
-                        Cc = rmax(Cd, Cc) + tv;              // eq:time
-                    }
-                    acc += Cc;                               // T_n = C_{n,M}
-                }
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                acc = __shfl_sync(0xffffffffu, acc, 0);      // warp-uniform decision
-                ++plans;
-                bsteps += (unsigned long long)N * M;
-                if (acc < best) { best = acc; bg = g; bm = mask; }   // (gamma, mask) ascend within a warp
+                acc += Cc;                               // T_n = C_{n,M}
             }
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            acc = __shfl_sync(0xffffffffu, acc, 0);      // warp-uniform decision
+            ++plans;
+            bsteps += (unsigned long long)G.N * M;
+            if (acc < best) { best = acc; bg = g0 + gi; bm = mask; }
         }
         if (lane == 0) { wv[warp] = best; wgs[warp] = bg; wm[warp] = bm; }
         __syncthreads();

@@ -33,9 +33,12 @@ def main():
     ap.add_argument("--n", type=int, default=2000)
     ap.add_argument("--pair", default="68M-7B")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mem", type=float, default=0, help="Gamma_s in bytes (0 = Table default)")
     ap.add_argument("--oracle", type=int, default=4, help="scenarios timed on the CPU oracle (0 = skip)")
     a = ap.parse_args()
     pd = scengen.params(a.pair, K=a.K, gamma_min=1, gamma_max=a.gmax)
+    if a.mem > 0:
+        pd["mem_capacity_bytes"] = int(a.mem)
     sc = scengen.generate(21, a.K, 0, a.n)
     I = torch.from_numpy(sc["I"]).cuda()
     al = torch.from_numpy(sc["alpha"]).cuda()
@@ -66,7 +69,7 @@ def main():
     ok = (o["status"].cpu().numpy() == 0) & (s1["status"].cpu().numpy() == 0)
     gap = (t1[ok] - tb[ok]) / tb[ok]
     ops = w[1] * OPS_PER_BATCH_STEP
-    res = dict(kernel="brute_force_kernel", K=a.K, gamma=[1, a.gmax], pair=a.pair, n=a.n,
+    res = dict(kernel="bf_item_kernel", K=a.K, mem_capacity_bytes=pd["mem_capacity_bytes"], gamma=[1, a.gmax], pair=a.pair, n=a.n,
                bf_scenarios_per_s=a.n / t_bf, bf_ms=t_bf * 1e3, plans_per_launch=int(w[0]),
                batch_steps_per_launch=int(w[1]),
                roofline=dict(bound="alu", achieved=ops / t_bf / 1e12, peak=PEAK / 1e12,
