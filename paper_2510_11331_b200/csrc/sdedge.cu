@@ -1940,16 +1940,30 @@ bf_item_kernel(const Consts C, const Inputs in, long long items, int gc, double*
             const BFGam G = gms[gi];
             const BFCoef* rg = rcs + gi * K;
             double acc = 0.0;
-            for (int step = 1 + lane; step <= G.N; step += 32) {
-                const double x = step - 1;
+            if (lane == 0) {                             // step n = 1 (prefill + first drafts), peeled
                 double Cd = 0.0, Cc = 0.0;
                 for (unsigned m = ends, st = 1; m; m &= m - 1) {
                     const int e = __ffs(m);
                     const double b = e - (int)st + 1;
                     st = e + 1;
-                    const BFCoef r = rg[e - 1];          // padded to the batch's longest input
-                    const double td = step == 1 ? fma(b, r.td1, G.c2dg) : fma(b * G.bdc, x, fma(b, r.ad, G.c2dg));
-                    const double tv = step == 1 ? fma(b, r.tv1, G.c2vv) : fma(b * G.bvc, x, fma(b, r.av, G.c2vv));
+                    const double td = fma(b, rg[e - 1].td1, G.c2dg), tv = fma(b, rg[e - 1].tv1, G.c2vv);
+                    if (nopipe) { Cc += td + tv; continue; }
+                    Cd += td;
+                    Cc = rmax(Cd, Cc) + tv;
+                }
+                acc = Cc;
+            }
+            for (int step = lane == 0 ? 33 : 1 + lane; step <= G.N; step += 32) {
+                const double x = step - 1;
+                const double xd = G.bdc * x, xv = G.bvc * x;    // slopes in n of the per-task stage times
+                double Cd = 0.0, Cc = 0.0;
+                for (unsigned m = ends, st = 1; m; m &= m - 1) {
+                    const int e = __ffs(m);
+                    const double b = e - (int)st + 1;
+                    st = e + 1;
+                    const BFCoef& r = rg[e - 1];         // padded to the batch's longest input
+                    const double td = fma(b, r.ad + xd, G.c2dg);   // T^d_n = b (ad + bdc (n-1)) + gamma c2d
+                    const double tv = fma(b, r.av + xv, G.c2vv);   // T^v_n = b (av + bvc (n-1)) + c2v
                     if (nopipe) { Cc += td + tv; continue; }
                     Cd += td;                            // C^d_{n,m}
                     Cc = rmax(Cd, Cc) + tv;              // eq:time

@@ -2,9 +2,10 @@
 NEXT-4 (i)) and of Algorithm 1 on the same scenarios, with the heuristic gap.
 
 Work model: per batch-step (one batch of one plan at one
-decoding step) the kernel does 9 fp64 lane-ops (2 FMAs + 1 mul per stage
-time x 2 stages, the C^d add, the max and the add of eq:time); the kernel
-counts the batch-steps it evaluated.  Timed with CUDA events on the
+decoding step) 7 fp64 lane-ops: each stage time b (a + s (n-1)) + c as one
+add and one FMA (the slope term s (n-1) is per step, not per batch), then
+the C^d add, the max and the add of eq:time; the kernel counts the
+batch-steps it evaluated.  Timed with CUDA events on the
 launching stream after warm-up; the oracle's exhaustive search is timed on
 a few scenarios on the host for context.
 
@@ -22,7 +23,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_11331_b200 as sd  # noqa: E402
 import scengen  # noqa: E402
 
-OPS_PER_BATCH_STEP = 9
+OPS_PER_BATCH_STEP = 7
 PEAK = 148 * 64 * 1.965e9   # fp64 lane-ops/s, DESIGN.md 7
 
 
