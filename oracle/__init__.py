@@ -79,6 +79,9 @@ def lib():
         L.orc_dp.restype = C.c_double
         L.orc_dp.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_f64,
                              P_i64, C.c_int, C.c_int]
+        L.orc_dp_trace.restype = C.c_double
+        L.orc_dp_trace.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_i32, P_f64,
+                                   P_f64, P_f64, P_i64]
         L.orc_eval_plan_nopipe.restype = C.c_double
         L.orc_eval_plan_nopipe.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, C.c_int, P_i32]
         L.orc_dp_nopipe.restype = C.c_double
@@ -194,6 +197,26 @@ def dp(pd, Is, alpha, gamma, coeffs=None, force_row=0, force_j=0):
     t = lib().orc_dp(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma,
                      _p(S, C.c_int32), _p(gap, C.c_double), C.byref(W), force_row, force_j)
     return t, S, gap, W.value
+
+
+def dp_trace(pd, Is, alpha, gamma, force=None, coeffs=None):
+    """Algorithm 1 for one gamma with row i taking j = force[i-1] where that is
+    > 0 (near-tie branching replay, SURVEY 8(c) "T"); returns
+    (T_inf, S, row_gap, row_best, row_taken, W)."""
+    K = len(Is)
+    P = make_params(dict(pd, K=K))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    f = None if force is None else np.ascontiguousarray(force, dtype=np.int32)
+    S = np.zeros(K, np.int32)
+    gap = np.full(K, np.inf)
+    rb = np.full(K, np.nan)
+    rt = np.full(K, np.nan)
+    W = C.c_int64(0)
+    co = _co(coeffs)
+    t = lib().orc_dp_trace(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, gamma, _p(f, C.c_int32),
+                           _p(S, C.c_int32), _p(gap, C.c_double), _p(rb, C.c_double), _p(rt, C.c_double),
+                           C.byref(W))
+    return t, S, gap, rb, rt, W.value
 
 
 def eval_plan_nopipe(pd, Is, alpha, gamma, batch_end, coeffs=None):

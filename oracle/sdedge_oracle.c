@@ -322,9 +322,17 @@ int orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is, dou
 
 /* Algorithm 1 with readings A1 (bracket of eq:t_ij1), A3 (K+1
  * rows, row 0 = 0, best = +inf), A4 (S[i] always set), A6 (largest j wins
- * ties: the ">=" of line 21). */
-double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
-              int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j)
+ * ties: the ">=" of line 21).
+ * force (optional, [K], 0 = free): row i takes j = force[i-1] instead of its
+ * argmin -- every candidate is still evaluated, so row_best[i-1] receives the
+ * row's minimum and row_taken[i-1] the value of the candidate taken.  This is
+ * the near-tie branching replay of SURVEY 8(c) "T": a plan reached by taking,
+ * at rows whose best-vs-taken gap is below a threshold, a near-best candidate
+ * instead of the best (PAPER.md:738 -- the tie rule decides exact ties only).
+ * A forced j that is memory-infeasible (or outside 1..i) makes the result NaN. */
+double orc_dp_trace(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                    const int32_t* force, int32_t* S, double* row_gap, double* row_best,
+                    double* row_taken, int64_t* W)
 {
     const int K = P->K;
     double L = orc_expected_tokens(alpha, gamma);
@@ -336,11 +344,11 @@ double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double a
 #define UPS(i, n, s) Y[(size_t)(i) * rowlen + (size_t)(n) * 2 + (s)]
     double result = 0.0;
     for (int i = 1; i <= K; ++i) {
-        double best = INFINITY, second = INFINITY;
+        double best = INFINITY, second = INFINITY, taken = NAN;
         int jstar = 0;
+        const int jf = force ? force[i - 1] : 0;
         int32_t Im = Is[i - 1]; /* max input length of tasks j..i */
         for (int j = 1; j <= i; ++j) {
-            if (i == force_row && j != force_j) continue;
             int b = i - j + 1;
             if (!batch_fits(P, b, Im)) continue; /* Alg. 1 lines 10-13 */
             for (int n = 1; n <= N; ++n) {      /* Alg. 1 lines 14-15 */
@@ -354,28 +362,51 @@ double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double a
                 temp += (d0 > y1 ? d0 : y1) + Tv[n];
             }
             if (W) *W += N;
+            if (j == jf) taken = temp;
             if (best >= temp) { second = best; best = temp; jstar = j; } /* line 21 */
             else if (temp < second) second = temp;
         }
         if (jstar == 0) { result = INFINITY; if (S) S[i - 1] = 0; break; } /* no feasible batch */
-        UPS(i, 0, 0) = best;                    /* eq:rg */
-        if (S) S[i - 1] = jstar;
+        if (jf > 0) {
+            if (isnan(taken)) { result = NAN; if (S) S[i - 1] = jf; break; } /* forced j infeasible */
+        } else {
+            taken = best;
+        }
+        const int jt = jf > 0 ? jf : jstar;
+        UPS(i, 0, 0) = taken;                   /* eq:rg (the taken candidate) */
+        if (S) S[i - 1] = jt;
         if (row_gap) /* relative gap; an exact tie is a zero gap even at best == 0 */
             row_gap[i - 1] = isinf(second) ? INFINITY : second == best ? 0.0 : (second - best) / fabs(best);
-        int b = i - jstar + 1;
+        if (row_best) row_best[i - 1] = best;
+        if (row_taken) row_taken[i - 1] = taken;
+        int b = i - jt + 1;
         for (int n = 1; n <= N; ++n) {          /* eq:tt1, eq:tt2 (line 26) */
             double td = orc_draft_time(P, co, b, Im, gamma, L, n);
             double tv = orc_verify_time(P, co, b, Im, gamma, L, n);
-            double d0 = UPS(jstar - 1, n, 0) + td;
-            double y1 = UPS(jstar - 1, n, 1);
+            double d0 = UPS(jt - 1, n, 0) + td;
+            double y1 = UPS(jt - 1, n, 1);
             UPS(i, n, 0) = d0;
             UPS(i, n, 1) = (d0 > y1 ? d0 : y1) + tv;
         }
-        result = best;
+        result = taken;
     }
 #undef UPS
     free(Y); free(Td); free(Tv);
     return result;
+}
+
+/* Algorithm 1 as written: orc_dp_trace with every row free, or with one
+ * forced row (force_row >= 1 takes j = force_j there). */
+double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+              int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j)
+{
+    if (force_row < 1 || force_row > P->K)
+        return orc_dp_trace(P, co, Is, alpha, gamma, NULL, S, row_gap, NULL, NULL, W);
+    int32_t* f = (int32_t*)calloc((size_t)P->K, sizeof(int32_t));
+    f[force_row - 1] = force_j;
+    double t = orc_dp_trace(P, co, Is, alpha, gamma, f, S, row_gap, NULL, NULL, W);
+    free(f);
+    return t;
 }
 
 /* Stable ascending sort of task indices by I_k (reading A13). */

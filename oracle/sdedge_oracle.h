@@ -73,10 +73,20 @@ double  orc_eval_plan(const orc_params* P, const double* co, const int32_t* Is, 
 /* Algorithm 1 for one gamma over sorted lengths Is[0..K-1].
  * S[K] receives 1-based boundaries; returns Upsilon[K,0,0] (+inf if infeasible).
  * row_gap[K] (optional) receives per-row relative gaps (+inf if < 2 candidates).
- * force_row/force_j (optional, force_row < 1 disables) forces the choice j at
- * one row -- used by the near-tie branching replay. */
+ * force_row/force_j (optional, force_row < 1 disables) makes row force_row take
+ * j = force_j (all candidates are still evaluated) -- see orc_dp_trace. */
 double  orc_dp(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
                int32_t* S, double* row_gap, int64_t* W, int force_row, int force_j);
+
+/* Near-tie branching replay (SURVEY 8(c) "T"): Algorithm 1 where row i takes
+ * j = force[i-1] when that is > 0 (force may be NULL: all rows free).  Every
+ * candidate of every row is evaluated as in orc_dp; row_best[K] receives each
+ * row's minimum candidate value, row_taken[K] the value of the candidate taken
+ * (the new Upsilon[i,0,0]).  Returns Upsilon[K,0,0] of the forced chain, +inf if
+ * some row has no feasible candidate, NaN if a forced j is infeasible. */
+double  orc_dp_trace(const orc_params* P, const double* co, const int32_t* Is, double alpha, int gamma,
+                     const int32_t* force, int32_t* S, double* row_gap, double* row_best,
+                     double* row_taken, int64_t* W);
 
 /* "SD w/o pipeline" evaluation of a plan: every decoding step runs draft then
  * verify of each batch sequentially, T_n = sum_m (T^d_{n,m} + T^v_{n,m}). */

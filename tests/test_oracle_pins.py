@@ -311,6 +311,51 @@ def test_dp_vs_brute_force(orc):
     assert n_eq > 0 and n_vd > 0
 
 
+def test_dp_trace_forced_chains(orc):
+    """Near-tie branching replay (SURVEY 8(c) "T"): orc_dp_trace with a force
+    vector.  Pinned against (i) the free DP (force = its own S gives the same
+    chain, row_taken == row_best everywhere), (ii) the literal eq:time
+    evaluation of the backtracked plan of ANY forced chain (P6: the taken chain
+    is that plan's pipeline state), (iii) brute force: the minimum over forced
+    chains whose plan is each contiguous partition equals the exhaustive optimum,
+    and row_best <= row_taken at every row."""
+    rng = np.random.default_rng(21)
+    for K in (1, 3, 5, 6):
+        for pd, co, Is, a in _instances(rng, 6, K):
+            for g in (1, 4):
+                t0, S0, gap0, W0 = orc.dp(pd, Is, a, g, coeffs=co)
+                t1, S1, gap1, rb1, rt1, W1 = orc.dp_trace(pd, Is, a, g, force=S0, coeffs=co)
+                assert t1 == t0 and list(S1) == list(S0) and W1 == W0
+                assert np.array_equal(rb1, rt1) and np.array_equal(gap0, gap1)
+                best_forced = np.inf
+                for mask in range(1 << (K - 1)):
+                    plan = [t + 1 for t in range(K - 1) if mask >> t & 1] + [K]
+                    f = np.zeros(K, np.int32)
+                    st = 1
+                    for e in plan:
+                        f[e - 1] = st
+                        st = e + 1
+                    # rows off the plan take a random memory-feasible j: they do not enter the plan's state
+                    for r in range(1, K + 1):
+                        if f[r - 1] == 0:
+                            j = int(rng.integers(1, r + 1))
+                            fits = np.isfinite(orc.eval_plan(dict(pd, K=r - j + 1), Is[j - 1:r], a, g, [r - j + 1],
+                                                             coeffs=co))
+                            f[r - 1] = j if fits else 0
+                    ev = orc.eval_plan(pd, Is, a, g, plan, coeffs=co)
+                    t, S, gap, rb, rt, W = orc.dp_trace(pd, Is, a, g, force=f, coeffs=co)
+                    assert np.isnan(t) == (not np.isfinite(ev))   # NaN exactly when a forced batch overflows
+                    if np.isfinite(ev):
+                        assert orc.backtrack(S) == plan
+                        assert rel(t, ev) < 1e-12
+                        ok = np.isfinite(rt)
+                        assert np.all(rb[ok] <= rt[ok])
+                        best_forced = min(best_forced, t)
+                bf, _, _ = orc.brute_force(pd, Is, a, g, g, coeffs=co)
+                if np.isfinite(bf):
+                    assert rel(best_forced, bf) < 1e-12
+
+
 def test_dp_counterexample_regression(orc):
     """Algorithm 1 returns the suboptimal {1}{2}{3}."""
     gd = gold("survey_B1_counterexample.json")
