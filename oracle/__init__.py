@@ -92,14 +92,18 @@ def lib():
         L.orc_eval_actual.argtypes = [C.POINTER(Params), P_f64, P_i32, P_i32, C.c_double, C.c_int, C.c_int, P_i32]
         L.orc_solve.restype = None
         L.orc_solve.argtypes = [C.POINTER(Params), P_i32, P_f64, P_f64, C.c_double, P_f64,
-                                C.POINTER(Result), P_i32, P_i32, P_f64, P_f64]
+                                C.POINTER(Result), P_i32, P_i32, P_f64, P_f64, P_i32]
+        L.orc_eval_plan_pbg.restype = C.c_double
+        L.orc_eval_plan_pbg.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, P_i32, P_i32]
+        L.orc_dp_pbg.restype = C.c_double
+        L.orc_dp_pbg.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, P_i32, P_i32, P_f64, P_i64]
         L.orc_brute_force.restype = C.c_double
         L.orc_brute_force.argtypes = [C.POINTER(Params), P_f64, P_i32, C.c_double, C.c_int, C.c_int,
                                       P_i32, P_i32, P_i32]
         L.orc_solve_batch.restype = None
         L.orc_solve_batch.argtypes = [C.POINTER(Params), C.c_int64, P_i32, P_f64, P_f64, P_f64, P_f64,
                                       P_i32, P_i32, P_i32, P_f64, P_i32, P_i32, P_f64, P_f64, P_f64,
-                                      P_i64, C.c_int]
+                                      P_i64, P_i32, C.c_int]
     return _lib
 
 
@@ -219,6 +223,32 @@ def dp_trace(pd, Is, alpha, gamma, force=None, coeffs=None):
     return t, S, gap, rb, rt, W.value
 
 
+def eval_plan_pbg(pd, Is, alpha, batch_end, gammas, coeffs=None):
+    """Planned T_inf of a plan with a speculation length per batch (NEXT-3 extension)."""
+    P = make_params(dict(pd, K=len(Is)))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    be = np.ascontiguousarray(batch_end, dtype=np.int32)
+    gm = np.ascontiguousarray(gammas, dtype=np.int32)
+    co = _co(coeffs)
+    return lib().orc_eval_plan_pbg(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, len(be),
+                                   _p(be, C.c_int32), _p(gm, C.c_int32))
+
+
+def dp_pbg(pd, Is, alpha, coeffs=None):
+    """Algorithm 1 over (j, gamma) candidates; returns (T_inf, S, Gm, row_gap, W)."""
+    K = len(Is)
+    P = make_params(dict(pd, K=K))
+    Is = np.ascontiguousarray(Is, dtype=np.int32)
+    S = np.zeros(K, np.int32)
+    Gm = np.zeros(K, np.int32)
+    gap = np.full(K, np.inf)
+    W = C.c_int64(0)
+    co = _co(coeffs)
+    t = lib().orc_dp_pbg(C.byref(P), _p(co, C.c_double), _p(Is, C.c_int32), alpha, _p(S, C.c_int32),
+                         _p(Gm, C.c_int32), _p(gap, C.c_double), C.byref(W))
+    return t, S, Gm, gap, W.value
+
+
 def eval_plan_nopipe(pd, Is, alpha, gamma, batch_end, coeffs=None):
     P = make_params(dict(pd, K=len(Is)))
     Is = np.ascontiguousarray(Is, dtype=np.int32)
@@ -281,12 +311,14 @@ def solve(pd, I, p, g, alpha, coeffs=None):
     be = np.zeros(K, np.int32)
     w = np.zeros(K)
     tg = np.zeros(pd["gamma_max"] - pd["gamma_min"] + 1)
+    bg = np.zeros(K, np.int32)
     lib().orc_solve(C.byref(P), _p(I, C.c_int32), _p(p, C.c_double), _p(g, C.c_double), alpha,
                     _p(co, C.c_double), C.byref(R), _p(order, C.c_int32), _p(be, C.c_int32),
-                    _p(w, C.c_double), _p(tg, C.c_double))
+                    _p(w, C.c_double), _p(tg, C.c_double), _p(bg, C.c_int32))
     return dict(status=R.status, gamma=R.gamma, M=R.M, T=R.T, T_com=R.T_com, T_inf=R.T_inf,
                 min_row_gap=R.min_row_gap, gap_gamma=R.gap_gamma, gap_row=R.gap_row,
-                gamma_gap=R.gamma_gap, W=R.W, order=order, batch_end=be, w=w, tinf_gamma=tg)
+                gamma_gap=R.gamma_gap, W=R.W, order=order, batch_end=be, w=w, tinf_gamma=tg,
+                batch_gamma=bg)
 
 
 def brute_force(pd, Is, alpha, gamma_min, gamma_max, coeffs=None):
@@ -313,7 +345,8 @@ def solve_batch(pd, sc, nthreads=None):
     out = dict(status=np.zeros(n, np.int32), gamma=np.zeros(n, np.int32), M=np.zeros(n, np.int32),
                lat=np.zeros((n, 3)), order=np.zeros((n, K), np.int32),
                batch_end=np.zeros((n, K), np.int32), w=np.zeros((n, K)),
-               min_row_gap=np.zeros(n), gamma_gap=np.zeros(n), W=np.zeros(n, np.int64))
+               min_row_gap=np.zeros(n), gamma_gap=np.zeros(n), W=np.zeros(n, np.int64),
+               batch_gamma=np.zeros((n, K), np.int32))
     nthreads = nthreads or os.cpu_count() or 1
     lib().orc_solve_batch(C.byref(P), n, _p(I, C.c_int32), _p(p, C.c_double), _p(g, C.c_double),
                           _p(al, C.c_double), _p(co, C.c_double), _p(out["status"], C.c_int32),
@@ -321,6 +354,6 @@ def solve_batch(pd, sc, nthreads=None):
                           _p(out["lat"], C.c_double), _p(out["order"], C.c_int32),
                           _p(out["batch_end"], C.c_int32), _p(out["w"], C.c_double),
                           _p(out["min_row_gap"], C.c_double), _p(out["gamma_gap"], C.c_double),
-                          _p(out["W"], C.c_int64), nthreads)
+                          _p(out["W"], C.c_int64), _p(out["batch_gamma"], C.c_int32), nthreads)
     out["nthreads"] = nthreads
     return out

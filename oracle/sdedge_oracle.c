@@ -409,6 +409,116 @@ double orc_dp(const orc_params* P, const double* co, const int32_t* Is, double a
     return t;
 }
 
+/* ---------------------------------------------------------------- per-batch gamma
+ * an EXTENSION, not the paper's method: the paper fixes one
+ * global speculation length l (cons. (f) P:555; the enumeration of P3),
+ * and SPEC.md:540 lists per-batch lengths as a non-goal.  Here batch m runs gamma_m
+ * draft passes per step, so it has its own L_m = eq:ol(alpha, gamma_m) and
+ * n_m = ceil(O_max / L_m) (eq:step_n under uniform O_max planning), and
+ * at step n only the batches with n_m >= n take part in the eq:time recursion --
+ * the active set M_n of eq:latency_infer_batch, the same mechanism the
+ * paper uses for batches that finish early.  Reading NB1: a row's
+ * candidates are the pairs (j, gamma); ties go to the largest j, then the
+ * smallest gamma. */
+double orc_eval_plan_pbg(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                         int M, const int32_t* batch_end, const int32_t* gammas)
+{
+    double* L = (double*)malloc(sizeof(double) * (M > 0 ? M : 1));
+    int* nm = (int*)malloc(sizeof(int) * (M > 0 ? M : 1));
+    int N = 0;
+    for (int m = 0; m < M; ++m) {
+        int start = m ? batch_end[m - 1] + 1 : 1;
+        if (!batch_fits(P, batch_end[m] - start + 1, Is[batch_end[m] - 1])) { free(L); free(nm); return INFINITY; }
+        L[m] = orc_expected_tokens(alpha, gammas[m]);
+        nm[m] = orc_decode_steps(P->O_max, L[m]);
+        if (nm[m] > N) N = nm[m];
+    }
+    double Tinf = 0.0;
+    for (int n = 1; n <= N; ++n) {
+        double Cd = 0.0, C = 0.0;
+        for (int m = 0; m < M; ++m) {
+            if (nm[m] < n) continue;                  /* active set M_n */
+            int start = m ? batch_end[m - 1] + 1 : 1;
+            int b = batch_end[m] - start + 1;
+            int32_t Im = Is[batch_end[m] - 1];
+            Cd += orc_draft_time(P, co, b, Im, gammas[m], L[m], n);
+            double st = Cd > C ? Cd : C;
+            C = st + orc_verify_time(P, co, b, Im, gammas[m], L[m], n);
+        }
+        Tinf += C;                                    /* T_n = C_{n, M_n} */
+    }
+    free(L); free(nm);
+    return Tinf;
+}
+
+/* Algorithm 1 (readings A1-A6) with candidates (j, gamma), gamma in
+ * [gamma_min, gamma_max]: Upsilon rows run over n = 1..N_max = max_gamma N_gamma; a
+ * candidate whose batch is finished at step n (n > N_gamma) adds no stage time there,
+ * max{Upsilon[j-1,n,0] + 0, Upsilon[j-1,n,1]} + 0 = Upsilon[j-1,n,1] (Upsilon1 >=
+ * Upsilon0 always).  S[i-1] = j*, Gm[i-1] = gamma* of the batch ending at row i. */
+double orc_dp_pbg(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                  int32_t* S, int32_t* Gm, double* row_gap, int64_t* W)
+{
+    const int K = P->K, ng = P->gamma_max - P->gamma_min + 1;
+    double* Lg = (double*)malloc(sizeof(double) * ng);
+    int* Ng = (int*)malloc(sizeof(int) * ng);
+    int N = 0;
+    for (int q = 0; q < ng; ++q) {
+        Lg[q] = orc_expected_tokens(alpha, P->gamma_min + q);
+        Ng[q] = orc_decode_steps(P->O_max, Lg[q]);
+        if (Ng[q] > N) N = Ng[q];
+    }
+    size_t rowlen = (size_t)(N + 1) * 2;
+    double* Y = (double*)calloc((size_t)(K + 1) * rowlen, sizeof(double));
+#define UPS(i, n, s) Y[(size_t)(i) * rowlen + (size_t)(n) * 2 + (s)]
+    double result = 0.0;
+    for (int i = 1; i <= K; ++i) {
+        double best = INFINITY, second = INFINITY;
+        int jstar = 0, qstar = -1;
+        int32_t Im = Is[i - 1];
+        for (int j = 1; j <= i; ++j) {
+            int b = i - j + 1;
+            if (!batch_fits(P, b, Im)) continue;
+            for (int q = ng - 1; q >= 0; --q) {           /* gamma descending: ties -> smallest gamma */
+                const int gm = P->gamma_min + q;
+                double temp = 0.0;
+                for (int n = 1; n <= N; ++n) {
+                    double y1 = UPS(j - 1, n, 1);
+                    if (n <= Ng[q]) {
+                        double d0 = UPS(j - 1, n, 0) + orc_draft_time(P, co, b, Im, gm, Lg[q], n);
+                        temp += (d0 > y1 ? d0 : y1) + orc_verify_time(P, co, b, Im, gm, Lg[q], n);
+                    } else {
+                        temp += y1;                       /* batch finished: no stage time */
+                    }
+                }
+                if (W) *W += N;
+                if (best >= temp) { second = best; best = temp; jstar = j; qstar = q; }
+                else if (temp < second) second = temp;
+            }
+        }
+        if (jstar == 0) { result = INFINITY; if (S) S[i - 1] = 0; if (Gm) Gm[i - 1] = -1; break; }
+        UPS(i, 0, 0) = best;
+        if (S) S[i - 1] = jstar;
+        if (Gm) Gm[i - 1] = P->gamma_min + qstar;
+        if (row_gap)
+            row_gap[i - 1] = isinf(second) ? INFINITY : second == best ? 0.0 : (second - best) / fabs(best);
+        const int b = i - jstar + 1, gm = P->gamma_min + qstar;
+        for (int n = 1; n <= N; ++n) {
+            double d0 = UPS(jstar - 1, n, 0), y1 = UPS(jstar - 1, n, 1);
+            if (n <= Ng[qstar]) {
+                d0 += orc_draft_time(P, co, b, Im, gm, Lg[qstar], n);
+                y1 = (d0 > y1 ? d0 : y1) + orc_verify_time(P, co, b, Im, gm, Lg[qstar], n);
+            }
+            UPS(i, n, 0) = d0;
+            UPS(i, n, 1) = y1;
+        }
+        result = best;
+    }
+#undef UPS
+    free(Y); free(Lg); free(Ng);
+    return result;
+}
+
 /* Stable ascending sort of task indices by I_k (reading A13). */
 static void sort_tasks(int K, const int32_t* I, int32_t* order)
 {
@@ -423,7 +533,7 @@ static void sort_tasks(int K, const int32_t* I, int32_t* order)
 
 void orc_solve(const orc_params* P, const int32_t* I, const double* p, const double* g,
                double alpha, const double* coeffs4, orc_result* R, int32_t* order,
-               int32_t* batch_end, double* w, double* tinf_gamma)
+               int32_t* batch_end, double* w, double* tinf_gamma, int32_t* batch_gamma)
 {
     const int K = P->K;
     const int ng = P->gamma_max - P->gamma_min + 1;
@@ -431,6 +541,7 @@ void orc_solve(const orc_params* P, const int32_t* I, const double* p, const dou
     R->gamma = -1; R->min_row_gap = INFINITY; R->gamma_gap = INFINITY;
     R->gap_gamma = -1; R->gap_row = -1;
     for (int k = 0; k < K; ++k) batch_end[k] = 0;
+    if (batch_gamma) for (int k = 0; k < K; ++k) batch_gamma[k] = 0;
     sort_tasks(K, I, order);
 
     int bad_task = 0;
@@ -460,6 +571,33 @@ void orc_solve(const orc_params* P, const int32_t* I, const double* p, const dou
     int gbest = -1, Mbest = 0;
     int32_t* ends = (int32_t*)malloc(sizeof(int32_t) * (K + 1));
     int32_t* ends_best = (int32_t*)malloc(sizeof(int32_t) * (K + 1));
+    if (P->batch_policy == 6) {   /* per-batch gamma (NEXT-3 extension): one DP over (j, gamma) */
+        int32_t* Gm = (int32_t*)malloc(sizeof(int32_t) * K);
+        for (int r = 0; r < K; ++r) gap[r] = INFINITY;
+        double t = orc_dp_pbg(P, coeffs4, Is, alpha, S, Gm, gap, &R->W);
+        for (int q = 0; q < ng; ++q) tinf_gamma[q] = t;
+        for (int r = 0; r < K; ++r)
+            if (gap[r] < R->min_row_gap) { R->min_row_gap = gap[r]; R->gap_gamma = -1; R->gap_row = r + 1; }
+        if (isinf(t)) {
+            R->status = 1;
+            R->T = R->T_inf = INFINITY;
+        } else {
+            int tmp[1024 + 1], i = K, M = 0;
+            while (i > 0) { tmp[M++] = i; i = S[i - 1] - 1; }
+            for (int m = 0; m < M; ++m) {
+                batch_end[m] = tmp[M - 1 - m];
+                if (batch_gamma) batch_gamma[m] = Gm[batch_end[m] - 1];
+            }
+            R->M = M;
+            R->gamma = Gm[K - 1];          /* the last batch's length (batch_gamma has them all) */
+            R->T_inf = t;
+            R->T = R->T_com + t;
+        }
+        free(Gm);
+        free(ends); free(ends_best);
+        free(Is); free(S); free(Sbest); free(gap);
+        return;
+    }
     for (int gm = P->gamma_min; gm <= P->gamma_max; ++gm) { /* P3 */
         double t;
         int Mg = 0;
@@ -493,6 +631,7 @@ void orc_solve(const orc_params* P, const int32_t* I, const double* p, const dou
         R->T = R->T_com + R->T_inf;
         R->gamma_gap = isinf(second) ? INFINITY : (second - best) / best;
         for (int m = 0; m < Mbest; ++m) batch_end[m] = ends_best[m];
+        if (batch_gamma) for (int m = 0; m < Mbest; ++m) batch_gamma[m] = gbest;
         R->M = Mbest;
     }
     free(ends); free(ends_best);
@@ -528,7 +667,7 @@ double orc_brute_force(const orc_params* P, const double* co, const int32_t* Is,
 typedef struct {
     const orc_params* P; int64_t n; const int32_t* I; const double *p, *g, *alpha, *coeffs;
     int32_t *status, *gamma, *M; double* lat; int32_t *order, *batch_end; double* w;
-    double *min_row_gap, *gamma_gap; int64_t* W; int64_t next;
+    double *min_row_gap, *gamma_gap; int64_t* W; int32_t* batch_gamma; int64_t next;
 } batch_ctx;
 
 static void* batch_worker(void* arg)
@@ -542,7 +681,7 @@ static void* batch_worker(void* arg)
         orc_result R;
         orc_solve(c->P, c->I + s * K, c->p + s * K, c->g + s * K, c->alpha[s],
                   c->coeffs ? c->coeffs + s * 4 : NULL, &R, c->order + s * K,
-                  c->batch_end + s * K, c->w + s * K, tg);
+                  c->batch_end + s * K, c->w + s * K, tg, c->batch_gamma ? c->batch_gamma + s * K : NULL);
         c->status[s] = R.status; c->gamma[s] = R.gamma; c->M[s] = R.M;
         c->lat[3 * s] = R.T; c->lat[3 * s + 1] = R.T_com; c->lat[3 * s + 2] = R.T_inf;
         if (c->min_row_gap) c->min_row_gap[s] = R.min_row_gap;
@@ -557,10 +696,10 @@ void orc_solve_batch(const orc_params* P, int64_t n, const int32_t* I, const dou
                      const double* g, const double* alpha, const double* coeffs,
                      int32_t* status, int32_t* gamma, int32_t* M, double* lat,
                      int32_t* order, int32_t* batch_end, double* w, double* min_row_gap,
-                     double* gamma_gap, int64_t* W, int nthreads)
+                     double* gamma_gap, int64_t* W, int32_t* batch_gamma, int nthreads)
 {
     batch_ctx c = {P, n, I, p, g, alpha, coeffs, status, gamma, M, lat, order, batch_end, w,
-                   min_row_gap, gamma_gap, W, 0};
+                   min_row_gap, gamma_gap, W, batch_gamma, 0};
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
     pthread_t th[256];

@@ -35,7 +35,8 @@ typedef struct {
     int32_t bw_policy;           /* 0 optimal eq:opt_w, 1 uniform w_k = 1/K */
     int32_t batch_policy;        /* 0 Algorithm 1 (pipelined), 1 SD w/o pipeline,
                                     2 no batching, 3 static,
-                                    4 max batching, 5 heuristic */
+                                    4 max batching, 5 heuristic,
+                                    6 per-batch gamma (an extension) */
     int32_t static_batch;        /* batch size of policy 3                          */
 } orc_params;
 
@@ -110,11 +111,25 @@ int     orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is,
 double  orc_eval_actual(const orc_params* P, const double* co, const int32_t* Is, const int32_t* Os,
                         double alpha, int gamma, int M, const int32_t* batch_end);
 
+/* Per-batch speculation length (an EXTENSION: the paper fixes one l,
+ * P:555).  Batch m has its own gamma_m, L_m and n_m = ceil(O_max/L_m);
+ * step n runs the eq:time recursion over the active batches n_m >= n (eq:latency_infer_batch,
+ * P:519-525).  Returns T_inf, +inf if a batch does not fit the memory. */
+double  orc_eval_plan_pbg(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                          int M, const int32_t* batch_end, const int32_t* gammas);
+
+/* Algorithm 1 over candidates (j, gamma) (reading NB1: ties -> largest j, then smallest
+ * gamma); a finished batch adds no stage time.  S[i-1] = j*, Gm[i-1] = gamma* at row i. */
+double  orc_dp_pbg(const orc_params* P, const double* co, const int32_t* Is, double alpha,
+                   int32_t* S, int32_t* Gm, double* row_gap, int64_t* W);
+
 /* Full solve of problem P for one scenario.
- * order[K], batch_end[K], w[K], tinf_gamma[gamma_max-gamma_min+1] are caller-owned. */
+ * order[K], batch_end[K], w[K], tinf_gamma[gamma_max-gamma_min+1] are caller-owned;
+ * batch_gamma[K] (optional) receives each batch's gamma (gamma* for every batch unless
+ * batch_policy == 6; then R->gamma is the last batch's). */
 void    orc_solve(const orc_params* P, const int32_t* I, const double* p, const double* g,
                   double alpha, const double* coeffs4, orc_result* R, int32_t* order,
-                  int32_t* batch_end, double* w, double* tinf_gamma);
+                  int32_t* batch_end, double* w, double* tinf_gamma, int32_t* batch_gamma);
 
 /* Exhaustive search over every contiguous partition of the sorted order and
  * every gamma (K <= 20).  Returns best T_inf; writes its plan. */
@@ -127,7 +142,7 @@ void    orc_solve_batch(const orc_params* P, int64_t n, const int32_t* I, const 
                         const double* g, const double* alpha, const double* coeffs,
                         int32_t* status, int32_t* gamma, int32_t* M, double* lat /*[n*3]*/,
                         int32_t* order, int32_t* batch_end, double* w, double* min_row_gap,
-                        double* gamma_gap, int64_t* W, int nthreads);
+                        double* gamma_gap, int64_t* W, int32_t* batch_gamma, int nthreads);
 
 #ifdef __cplusplus
 }
