@@ -1,17 +1,20 @@
 #!/usr/bin/env python
 """Benchmark: scenarios solved per second (fp64) by the sm_100a solver.
 
-Workload (BASELINE.json configs[3]): 1e6 independent
-scenarios per GPU, K = 128 tasks, gamma 1..16, (LLaMA-68M, LLaMA-7B),
-alpha ~ U[0.5, 0.9), Rayleigh channels -- synthetic, seeded (scengen).
-One step = one sdedge_solve_batch over the rank's whole shard (every row of
-SURVEY 8(a): staging, sort, bandwidth, per-gamma DP, gamma argmin,
-backtrack).  Inputs (2.6 GB) exceed the 126 MB L2, so no flush is needed.
+Workload (BASELINE.json configs[3]): the 1e6-scenario sweep,
+K = 128 tasks, gamma 1..16, (LLaMA-68M, LLaMA-7B), alpha ~ U[0.5, 0.9),
+Rayleigh channels -- synthetic, seeded (scengen).  One step = one
+sdedge_solve_batch over the rank's shard (every row of SURVEY 8(a): staging,
+sort, bandwidth, per-gamma DP, gamma argmin, backtrack).  Inputs (2.6 GB)
+exceed the 126 MB L2, so no flush is needed.
 
     python bench.py [--gpus N --steps K --warmup W] [--algo envelope|dense]
-                    [--precision fp64|fp32] [--impl reference]
-Under torchrun (N > 1) each rank solves its own 1e6-scenario shard (weak
-scaling, no data-path collective); times are max over ranks.
+                    [--precision fp64|fp32] [--pair 1.1B-7B] [--impl reference]
+Under torchrun (N > 1): strong scaling by default -- rank r
+solves the contiguous shard [r c, (r+1) c), c = ceil(1e6 / N), and its outputs
+are gathered to cuda:0 inside the solve (the kernel stores them into cuda:0's
+arrays over NVLink through CUDA IPC: paper_2510_11331_b200/shard.py); times
+are max over ranks.  --scaling weak gives every rank its own 1e6 scenarios.
 """
 from __future__ import annotations
 
@@ -47,12 +50,46 @@ FP32_LANES_PER_SM = 128
 OPS = {"dense": dict(cand=16, seg=0, step=4, row=40, pruned=0),
        "envelope": dict(cand=16, seg=10, step=0, row=40, pruned=3)}
 
-# DRAM bytes (read + write) per scenario of the envelope kernel from the one
-# `ncu --set full` capture of round 1 (profiles/r01_ncu_envelope_final_c4.md:
-# 0.29 GB read + 0.91 GB written for a 1e5-scenario C4 launch), scaled to the
-# launch.  The algorithmic bytes are 2568 in + 2084 out per scenario; the rest
-# is the write-back of the tiled DP's global row store.
-NCU_DRAM_BYTES_PER_SCENARIO = {("C4", "envelope", "fp64"): (0.29304576e9 + 0.912838656e9) / 1e5}
+# DRAM bytes (read + write) per scenario of the main solve launch, from the
+# `ncu --set full` capture of THIS build (profiles/ncu_traffic.json, written by
+# tools/ncu_traffic.py with the sha256 of csrc/sdedge.cu it was measured on);
+# reported only when that sha matches the source being benchmarked.
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def measured_traffic(key: str):
+    import hashlib
+    try:
+        rec = json.load(open(TRAFFIC_JSON)).get(key)
+        src = open(os.path.join(ROOT, "paper_2510_11331_b200", "csrc", "sdedge.cu"), "rb").read()
+        if rec and rec["source_sha256"] == hashlib.sha256(src).hexdigest():
+            return rec
+    except Exception:
+        pass
+    return None
+
+
+def dense_work(pd, sc):
+    """W of SURVEY 8(d): the candidate-steps sum_gamma N_gamma sum_i |window(i)| the
+    paper's loop would execute for these scenarios (bookkeeping for
+    the dense-equivalent rate; the envelope kernel does not execute them)."""
+    a = np.asarray(sc["alpha"], dtype=np.float64)
+    K = pd["K"]
+    Jd, hd, h2d = pd["draft"]
+    Gp = Jd * (8 * hd * hd + 4 * hd * h2d)
+    Is = np.sort(np.asarray(sc["I"], dtype=np.int64), axis=1)
+    room = pd["mem_capacity_bytes"] - Gp
+    bmax = np.maximum(room, 0) // (4 * Jd * hd * (Is + pd["O_max"]))
+    win = np.minimum(bmax, np.arange(1, K + 1)[None, :]).sum(1).astype(np.float64)
+    W = np.zeros_like(a)
+    A = a.copy()
+    for g in range(0, pd["gamma_max"] + 1):
+        if g > 0:
+            A = A * a
+        if g >= pd["gamma_min"]:
+            L = (1.0 - A) / (1.0 - a)
+            W += np.ceil(pd["O_max"] / L) * win
+    return float(W.sum())
 
 
 def parse():
@@ -70,6 +107,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     return ap.parse_args()
 
 
@@ -190,7 +228,7 @@ def run_reference(args):
                pair=f"{scengen_pair(pd)}")
     line = {"impl": "reference", "metric": "scenarios solved/sec (fp64)", "value": value,
             "unit": "scenarios/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": value, "unit": "scenarios/s", "cores": cores, "kind": "oracle",
                              "cpu": cpu_model(),
@@ -213,6 +251,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2510_11331_b200 as sd
+    from paper_2510_11331_b200.shard import GatherLayout, shard_range
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -232,11 +271,18 @@ def main():
     dev = torch.device("cuda", local)
     sd.lib()
 
-    pd, _, n_total = scengen.config(args.config, 0, 1, pair=args.pair)
-    n = args.n or n_total
-    s0, _ = shard(rank, n)                                  # weak scaling: own shard per rank
+    pd, _, n_cfg = scengen.config(args.config, 0, 1, pair=args.pair)
+    strong = args.scaling == "strong"
+    if strong:
+        n_total = args.n or n_cfg
+        s0, s1 = shard_range(n_total, ws, rank)
+    else:
+        n_rank = args.n or n_cfg
+        n_total = n_rank * ws
+        s0, s1 = shard(rank, n_rank)
+    n = s1 - s0
     t_gen = time.perf_counter()
-    _, sc, _ = scengen.config(args.config, s0, s0 + n, pair=args.pair)
+    _, sc, _ = scengen.config(args.config, s0, s1, pair=args.pair)
     t_gen = time.perf_counter() - t_gen
     K = pd["K"]
     prec = 0 if args.precision == "fp64" else 1
@@ -246,14 +292,46 @@ def main():
     d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
     stream = torch.cuda.current_stream(dev)
     work = torch.zeros(5, dtype=torch.int64, device=dev)
-    out = sd._alloc_out(torch, n, K, dev, True)
+    local_out = sd._alloc_out(torch, n, K, dev, True)
 
-    def step(count=False):
+    # ---- the gathered outputs of all n_total scenarios live on cuda:0 (rank 0);
+    # every rank's solve stores its shard's rows there (fused NVLink gather)
+    lay = GatherLayout(n_total, K, True)
+    gbuf, gout, peer = None, local_out, None
+    if ws > 1 and strong:
+        if rank == 0:
+            gbuf = torch.empty(lay.nbytes, dtype=torch.uint8, device=dev)
+            h = [sd.ipc_export(gbuf)]
+        else:
+            h = [None]
+        dist.broadcast_object_list(h, src=0, device=dev)
+        if rank == 0:
+            gout = lay.rows(gbuf.data_ptr(), s0)
+        else:
+            peer = (sd.ipc_open(*h[0]), h[0][1])
+            gout = lay.rows(peer[0], s0)
+        dist.barrier()
+
+    def step(out, count=False):
         sd.solve(pd, d["I"], d["p"], d["g"], d["alpha"], None, out=out, stream=stream, precision=prec,
                  algo=algo, work_counters=work if count else None)
 
+    def timed(out, count, clk=None):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(out, count)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        return e0.elapsed_time(e1) * 1e-3
+
     for _ in range(args.warmup):
-        step()
+        step(gout)
     torch.cuda.synchronize()
     launches_per_step = sd.sdedge_last_launch_count()
 
@@ -263,23 +341,23 @@ def main():
         uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
     except Exception:
         pass
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     work.zero_()
     with ClockSampler(uuid) as clk:
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step(count=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-    el = e0.elapsed_time(e1) * 1e-3
+        el = timed(gout, True)
     el_max = max_over_ranks(el, dist, dev)
     wk = work.cpu().numpy().astype(np.float64) / args.steps    # per step (= per main launch)
-    status_ok = int((out["status"] == 0).sum().item())
+    solve_only = None
+    if ws > 1 and strong:
+        # the same shards with rank-local outputs: the cost of the fused gather
+        for _ in range(max(1, args.warmup // 2)):
+            step(local_out)
+        t_loc = max_over_ranks(timed(local_out, False), dist, dev)
+        solve_only = {"value": n_total / (t_loc / args.steps), "unit": "scenarios/s",
+                      "ms_per_step": 1e3 * t_loc / args.steps,
+                      "note": "outputs kept on each rank's GPU (no gather)"}
+    if rank == 0:
+        st = gout["status"] if ws == 1 or not strong else lay.views(torch, gbuf)["status"]
+        status_ok = int((st == 0).sum().item())
 
     # ---- end to end through the host entry point (pinned host in, pinned host out)
     e2e = None
@@ -292,7 +370,6 @@ def main():
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        h0 = time.perf_counter()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(ksteps):
@@ -303,21 +380,26 @@ def main():
         te = max_over_ranks(f0.elapsed_time(f1) * 1e-3, dist, dev)
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         d2h = sum(v.numel() * v.element_size() for v in hout.values() if v is not None)
-        e2e = {"value": n * ws * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d * ws,
-               "d2h_bytes_per_step": d2h * ws, "steps": ksteps, "entry": "sdedge_solve_batch_host"}
+        e2e = {"value": n_total * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h * ws, "steps": ksteps, "entry": "sdedge_solve_batch_host",
+               "note": "per-rank shard host->device->host; PCIe-bound (inputs alone are 2568 B/scenario)"}
 
-    # ---- roofline of the dominant kernel (solve_kernel<.., BIG=0>; the second
-    # launch is the worst-case-pool pass, empty unless an envelope overflowed)
+    # ---- roofline of the dominant kernel (solve_kernel main pass; the second launch
+    # is the worst-case-pool pass, empty unless an envelope overflowed)
     props = torch.cuda.get_device_properties(dev)
     nsm = props.multi_processor_count
     lanes = FP64_LANES_PER_SM if prec == 0 else FP32_LANES_PER_SM
-    peak = nsm * lanes * 1965e6
+    peak_derived = nsm * lanes * 1965e6
+    peak_meas, _ = sd.sdedge_pipe_peak(prec == 1)            # same run, after the timed region
     o = OPS[args.algo]
     ops = (o["cand"] * wk[4] + o["seg"] * wk[1] + o["step"] * wk[2] + o["row"] * wk[3]
            + o["pruned"] * (wk[0] - wk[4]))
     t_launch = el / args.steps
     achieved = ops / t_launch
+    W_full = dense_work(pd, sc)
     clocks = clk.summary()
+    tr_key = f"{args.config}/{scengen_pair(pd)}/{args.algo}/{args.precision}"
+    tr = measured_traffic(tr_key)
 
     if rank == 0:
         cpu = None
@@ -332,34 +414,47 @@ def main():
                 cpu = {"value": None, "unit": "scenarios/s", "cores": cores, "kind": "oracle",
                        "sample": f"failed: {e}"}
         cfg = config_of(args, n, ws)
-        cfg.update(K=K, gamma=[pd["gamma_min"], pd["gamma_max"]], pair=scengen_pair(pd))
+        cfg.update(K=K, gamma=[pd["gamma_min"], pd["gamma_max"]], pair=scengen_pair(pd),
+                   scenarios_per_gpu=n, total_scenarios=n_total,
+                   parallelism=(f"scenario-shard x{ws}" + (", outputs gathered to cuda:0 by the solve's own "
+                                                          "NVLink peer stores (CUDA IPC)" if ws > 1 and strong
+                                                          else "")))
         line = {
             "metric": "scenarios solved/sec (fp64)" if prec == 0 else "scenarios solved/sec (fp32 variant)",
-            "value": n * ws / (el_max / args.steps),
+            "value": n_total / (el_max / args.steps),
             "unit": "scenarios/s",
             "n_gpus": ws,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": 1e3 * el_max / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "f64" if prec == 0 else "f32",
             "data": "synthetic",
             "config": cfg,
-            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                         "unit": "T fp64-lane-ops/s" if prec == 0 else "T fp32-lane-ops/s",
-                         "frac": achieved / peak,
-                         "traffic": (NCU_DRAM_BYTES_PER_SCENARIO[(args.config, args.algo, args.precision)] * n
-                                     if (args.config, args.algo, args.precision) in NCU_DRAM_BYTES_PER_SCENARIO
-                                     else None),
-                         "traffic_unit": "DRAM bytes per launch (r01 ncu capture, per-scenario scaled)",
-                         "algorithmic_bytes": (20 * K + 8 + 36 + 16 * K) * n,
-                         "peak_source": f"derived: {nsm} SMs x {lanes} lanes x 1965 MHz (B200_PROFILING.md)",
-                         "work_per_launch": {"candidates": wk[0], "full_evaluations": wk[4],
-                                             "cand_segments": wk[1], "candidate_steps_W": wk[2],
-                                             "rows": wk[3], "ops": ops},
-                         "kernel": "solve_kernel (main pass)"},
+            "roofline": {
+                "bound": "alu", "achieved": achieved / 1e12, "peak": peak_meas / 1e12,
+                "unit": "T fp64-lane-ops/s" if prec == 0 else "T fp32-lane-ops/s",
+                "frac": achieved / peak_meas,
+                "traffic": (tr["dram_bytes_per_scenario"] * n) if tr else None,
+                "traffic_source": (f"ncu --set full of this build ({tr['capture']})" if tr else
+                                   "none for this build/config"),
+                "algorithmic_bytes": (20 * K + 8 + 36 + 16 * K) * n,
+                "op_model": "envelope op model (DESIGN.md 7): 16 per fully evaluated candidate, 10 per "
+                            "(candidate, predecessor segment), 3 per candidate pruned by the exact bound, "
+                            "40 per DP row -- the work the kernel executes after exact pruning",
+                "peak_source": f"sdedge_pipe_peak DFMA/FFMA chain on all {nsm} SMs, measured in this run "
+                               f"(derived {peak_derived / 1e12:.2f} T = {nsm} SMs x {lanes} lanes x 1965 MHz, "
+                               f"frac vs derived {achieved / peak_derived:.4f})",
+                "dense_equivalent": {"W": W_full, "ops": 4 * W_full, "rate": 4 * W_full / t_launch / 1e12,
+                                     "frac": 4 * W_full / t_launch / peak_meas,
+                                     "note": "SURVEY 8(d) 4 ops x W candidate-steps of the paper's O(K^2 N) "
+                                             "loop -- NOT executed: the envelope closed form and exact pruning "
+                                             "replace it, so this exceeds the peak"},
+                "work_per_launch": {"candidates": wk[0], "full_evaluations": wk[4], "cand_segments": wk[1],
+                                    "candidate_steps_W": wk[2], "rows": wk[3], "ops": ops},
+                "kernel": "solve_kernel (main pass)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -367,8 +462,13 @@ def main():
             "status_ok": status_ok,
             "gen_s": t_gen,
         }
+        if solve_only:
+            line["solve_only"] = solve_only
         print(json.dumps(line))
     if ws > 1:
+        dist.barrier()
+        if peer is not None:
+            sd.ipc_close(*peer)
         dist.barrier()
         dist.destroy_process_group()
 

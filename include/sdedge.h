@@ -29,7 +29,10 @@
  *     memory recommended); it stages the copies itself.
  *   - The call is asynchronous on params->stream (NULL = legacy default
  *     stream); results are valid once that stream completes.  Workspace is
- *     stream-ordered (cudaMallocAsync) and freed on the same stream.
+ *     stream-ordered (cudaMallocFromPoolAsync) and freed on the same stream;
+ *     it comes from a library-private memory pool per device (created on
+ *     first use, kept cached between calls) -- the device's default pool and
+ *     the caller's allocators are not touched.
  *   - Per-scenario problems never fail the call: they set status[s] and
  *     write gamma = -1, num_batches = 0, batch_end = 0 and
  *       status 1 (memory-infeasible: some task fits in no batch, cons. (b)
@@ -40,8 +43,8 @@
  *     order[] is always the stable sort; bw_share is valid for status 0-2.
  *   - Return: 0 = enqueued; -1 = invalid argument (see sdedge_last_error());
  *     -2 = CUDA error; -3 = out of device memory.
- *   - Thread-safe and re-entrant across streams and devices (no global
- *     mutable state besides the thread-local error string).
+ *   - Thread-safe and re-entrant across streams and devices (global state:
+ *     the thread-local error string and the mutex-guarded per-device pool).
  */
 #ifndef SDEDGE_H
 #define SDEDGE_H
@@ -51,7 +54,7 @@
 extern "C" {
 #endif
 
-#define SDEDGE_ABI_VERSION 2
+#define SDEDGE_ABI_VERSION 3
 #define SDEDGE_MAX_K 1024
 
 typedef struct {
@@ -83,7 +86,14 @@ typedef enum {
     SDEDGE_BATCH_NONE = 2,       /* "No batching": one task per batch, pipelined        */
     SDEDGE_BATCH_STATIC = 3,     /* fixed batch size `static_batch` in sorted order  */
     SDEDGE_BATCH_MAX = 4,        /* largest memory-feasible size for the longest input */
-    SDEDGE_BATCH_HEURISTIC = 5   /* sizes 2,3,... until the latency stops improving */
+    SDEDGE_BATCH_HEURISTIC = 5,  /* sizes 2,3,... until the latency stops improving */
+    SDEDGE_BATCH_PER_BATCH_GAMMA = 6 /* EXTENSION (not the paper's method, which fixes
+                                    one l): Algorithm 1 over candidates (j, gamma) --
+                                    every batch has its own gamma, L and N_gamma = ceil(O_max / L), and
+                                    step n runs only the batches with N_gamma >= n (the active set of
+                                    eq:latency_infer_batch).  Ties: largest j, then smallest
+                                    gamma.  fp64 only, <= 32 gammas, (K+1) O_max <= 2^27.  gamma[s] is
+                                    the last batch's; batch_gamma (below) has every batch's.         */
 } sdedge_batch_policy;
 
 typedef struct {
@@ -130,6 +140,15 @@ typedef struct {
                                     segments, candidate-steps sum N (the paper's O(K^2 N) work W),
                                     DP rows, candidates fully evaluated (the rest were pruned by the
                                     exact lower bound); NULL = not counted.  Ignored by _host.      */
+    int32_t* row_choice;         /* optional DEVICE [n*K] step trace (SPEC.md:422 debug export): Algorithm 1's
+                                    boundary vector S at gamma*, S[i-1] = the 1-based start j* chosen at
+                                    sorted row i for EVERY row (reading A4), not only the rows
+                                    the backtrack visits -- so the whole DP state of the answer can be
+                                    replayed (tests: near-tie branching replay, SURVEY 8(c) "T").  0 in
+                                    every entry where status != 0.  NULL = not written.  Ignored by _host. */
+    int32_t* batch_gamma;        /* optional DEVICE [n*K]: the speculation length of batch m (m < M), 0
+                                    for m >= M -- gamma* for every batch except under
+                                    SDEDGE_BATCH_PER_BATCH_GAMMA.  NULL = not written.  Ignored by _host. */
 } sdedge_schedule;
 
 /* Solve n scenarios.  out_latency: [n*3] = {T, T_com, T_inf} (seconds). */
@@ -150,8 +169,10 @@ int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const 
  * (or, under SDEDGE_BATCH_NO_PIPELINE, run draft then verify sequentially).
  * output_len: DEVICE [n*K] int32 >= 1 (original task order); plan: DEVICE
  * arrays gamma, num_batches, batch_end, order, status (others ignored);
- * out_t_inf: DEVICE [n] actual T_inf in seconds (NaN where status != 0 or
- * some O_k < 1).  Uses the same params (models, coefficients, K, O_max,
+ * out_t_inf: DEVICE [n] actual T_inf in seconds (NaN where status != 0,
+ * some O_k < 1, or the plan is malformed: batch_end not strictly increasing in
+ * 1..K with batch M-1 ending at K, an order entry outside 0..K-1, M outside
+ * 1..K, gamma outside 0..64).  Uses the same params (models, coefficients, K, O_max,
  * stream) as the solve.  Asynchronous; returns 0 / -1 / -2 like the solve. */
 int sdedge_evaluate_actual(const sdedge_scenarios* scenarios, const int32_t* output_len, int64_t n,
                            const sdedge_params* params, const sdedge_schedule* plan, double* out_t_inf);
@@ -174,6 +195,25 @@ int sdedge_evaluate_actual(const sdedge_scenarios* scenarios, const int32_t* out
  * workspace is stream-ordered.  Returns 0 / -1 / -2 / -3. */
 int sdedge_brute_force(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
                        double* out_t_inf, sdedge_schedule* out);
+
+/* Multi-GPU gather: one process per GPU solves a contiguous shard of
+ * the scenarios; the only exchange is the final gather of the outputs to cuda:0.
+ * It is fused into the solve: rank 0 exports its output allocation once, every
+ * other rank maps it and passes pointers into it (at its shard's rows) as the
+ * out_latency / out_schedule arrays of sdedge_solve_batch, so the solve kernel's
+ * epilogue stores each scenario's results over NVLink as it finishes -- no copy
+ * after the solve.
+ *   sdedge_ipc_export: dev_ptr = any address inside a cudaMalloc'd (e.g. torch)
+ *     allocation on the current device; writes the allocation's 64-byte CUDA IPC
+ *     handle to handle[0..63] and dev_ptr's byte offset in it to *offset.
+ *   sdedge_ipc_open: maps that allocation into this process (peer access enabled
+ *     lazily) and returns base + offset in *dev_ptr.  Unmap with sdedge_ipc_close
+ *     (same offset).  The exporter must keep the allocation alive meanwhile.
+ * Synchronous host calls; return 0, -1 (bad argument) or -2 (CUDA error). */
+#define SDEDGE_IPC_HANDLE_BYTES 64
+int sdedge_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
+int sdedge_ipc_open(const void* handle, uint64_t offset, void** dev_ptr);
+int sdedge_ipc_close(void* dev_ptr, uint64_t offset);
 
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int sdedge_last_launch_count(void);

@@ -18,11 +18,12 @@ __all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_act
 
 ALGO_ENVELOPE, ALGO_DENSE = 0, 1
 BW_OPTIMAL, BW_UNIFORM = 0, 1
-BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC = range(6)
+BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC, BATCH_PER_BATCH_GAMMA = range(7)
 FLAG_TINY_POOL = 1
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
                     "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
-                    "sdedge_abi_version", "sdedge_pipe_peak")
+                    "sdedge_abi_version", "sdedge_pipe_peak", "sdedge_ipc_export", "sdedge_ipc_open",
+                    "sdedge_ipc_close")
 
 
 class SdedgeModel(C.Structure):
@@ -49,7 +50,7 @@ class SdedgeScenarios(C.Structure):
 class SdedgeSchedule(C.Structure):
     _fields_ = [("gamma", C.c_void_p), ("num_batches", C.c_void_p), ("batch_end", C.c_void_p),
                 ("order", C.c_void_p), ("bw_share", C.c_void_p), ("status", C.c_void_p),
-                ("work_counters", C.c_void_p)]
+                ("work_counters", C.c_void_p), ("row_choice", C.c_void_p), ("batch_gamma", C.c_void_p)]
 
 
 _lib = None
@@ -77,6 +78,12 @@ def lib() -> C.CDLL:
         L.sdedge_last_error.restype = C.c_char_p
         L.sdedge_last_launch_count.restype = C.c_int
         L.sdedge_abi_version.restype = C.c_int
+        L.sdedge_ipc_export.restype = C.c_int
+        L.sdedge_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.sdedge_ipc_open.restype = C.c_int
+        L.sdedge_ipc_open.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.sdedge_ipc_close.restype = C.c_int
+        L.sdedge_ipc_close.argtypes = [C.c_void_p, C.c_uint64]
         L.sdedge_pipe_peak.restype = C.c_int
         L.sdedge_pipe_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib = L
@@ -118,9 +125,39 @@ def _ptr(t):
     return t.ctypes.data  # numpy (host entry point)
 
 
-def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, status, work=None):
+def _check(name, t, dtype, shape, device):
+    """Marshalling guard: the C ABI takes raw pointers, so a wrong dtype, a
+    non-contiguous view, a wrong device or shape would be read as garbage."""
+    if t is None:
+        return
+    import torch
+    if t.dtype != dtype or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: need a contiguous {dtype} tensor of shape {tuple(shape)}, "
+                         f"got {t.dtype} {tuple(t.shape)} contiguous={t.is_contiguous()}")
+    if device == "host" and t.is_cuda:
+        raise ValueError(f"{name}: the host entry point takes host (pinned) tensors")
+    if isinstance(device, torch.device) and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+
+
+def _check_inputs(I, p, g, alpha, coeffs, device):
+    import torch
+    if I.dim() != 2:
+        raise ValueError("I: need a [n, K] int32 tensor")
+    n, K = I.shape
+    _check("I", I, torch.int32, (n, K), device)
+    _check("p", p, torch.float64, (n, K), device)
+    _check("g", g, torch.float64, (n, K), device)
+    _check("alpha", alpha, torch.float64, (n,), device)
+    _check("coeffs", coeffs, torch.float64, (n, 4), device)
+    return n, K
+
+
+def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, status, work=None, trace=None,
+          bgam=None):
     sc = SdedgeScenarios(_ptr(I), _ptr(p), _ptr(g), _ptr(alpha), _ptr(coeffs))
-    sch = SdedgeSchedule(_ptr(gamma), _ptr(M), _ptr(bend), _ptr(order), _ptr(w), _ptr(status), _ptr(work))
+    sch = SdedgeSchedule(_ptr(gamma), _ptr(M), _ptr(bend), _ptr(order), _ptr(w), _ptr(status), _ptr(work),
+                         _ptr(trace), _ptr(bgam))
     rc = fn(C.byref(sc), n, C.byref(P), _ptr(lat), C.byref(sch))
     if rc != 0:
         raise RuntimeError(f"sdedge_solve_batch failed ({rc}): {sdedge_last_error()}")
@@ -128,10 +165,10 @@ def _call(fn, I, p, g, alpha, coeffs, n, P, lat, gamma, M, bend, order, w, statu
 
 
 def sdedge_solve_batch(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma, num_batches,
-                       batch_end, order, bw_share, status, work_counters=None):
+                       batch_end, order, bw_share, status, work_counters=None, row_choice=None, batch_gamma=None):
     """Direct C-ABI call on DEVICE tensors (all contiguous, see include/sdedge.h)."""
     return _call(lib().sdedge_solve_batch, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
-                 num_batches, batch_end, order, bw_share, status, work_counters)
+                 num_batches, batch_end, order, bw_share, status, work_counters, row_choice, batch_gamma)
 
 
 def sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma,
@@ -156,7 +193,8 @@ def sdedge_evaluate_actual(I, p, g, alpha, coeffs, output_len, n, params: Sdedge
 def evaluate_actual(params: dict, I, p, g, alpha, output_len, plan: dict, coeffs=None, stream=None):
     """Actual-output T_inf [n] (CUDA tensor) of the plans in `plan` (solve() output)."""
     import torch
-    n, K = I.shape
+    n, K = _check_inputs(I, p, g, alpha, coeffs, I.device)
+    _check("output_len", output_len, torch.int32, (n, K), I.device)
     if stream is None:
         stream = torch.cuda.current_stream(I.device)
     P = make_params(dict(params, K=K), stream=stream)
@@ -183,6 +221,9 @@ def brute_force(params: dict, I, alpha, coeffs=None, stream=None, work_counters=
     scenarios (K <= 20); returns CUDA tensors t_inf, gamma, M, batch_end, order, status."""
     import torch
     n, K = I.shape
+    _check("I", I, torch.int32, (n, K), I.device)
+    _check("alpha", alpha, torch.float64, (n,), I.device)
+    _check("coeffs", coeffs, torch.float64, (n, 4), I.device)
     if stream is None:
         stream = torch.cuda.current_stream(I.device)
     P = make_params(dict(params, K=K), stream=stream)
@@ -203,6 +244,43 @@ def sdedge_pipe_peak(fp32: bool = False):
     return ops.value, el.value
 
 
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    h = (C.c_ubyte * 64)()
+    off = C.c_uint64(0)
+    rc = lib().sdedge_ipc_export(t.data_ptr(), h, C.byref(off))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_ipc_export failed ({rc}): {sdedge_last_error()}")
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Map a peer allocation exported by ipc_export; returns the device address."""
+    h = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p(0)
+    rc = lib().sdedge_ipc_open(h, offset, C.byref(p))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_ipc_open failed ({rc}): {sdedge_last_error()}")
+    return p.value
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    rc = lib().sdedge_ipc_close(ptr, offset)
+    if rc != 0:
+        raise RuntimeError(f"sdedge_ipc_close failed ({rc}): {sdedge_last_error()}")
+
+
+class Rows:
+    """Raw device address of row `row` of a row-major [n, width] array of
+    `itemsize`-byte elements (peer-mapped output arrays carry no torch tensor)."""
+
+    def __init__(self, base: int, width: int, itemsize: int, row: int = 0):
+        self.addr = base + row * width * itemsize
+
+    def data_ptr(self) -> int:
+        return self.addr
+
+
 def _alloc_out(torch, n, K, device, want_w, pin=False):
     kw = dict(device=device) if device is not None else dict(pin_memory=pin)
     return dict(lat=torch.empty((n, 3), dtype=torch.float64, **kw),
@@ -215,18 +293,26 @@ def _alloc_out(torch, n, K, device, want_w, pin=False):
 
 
 def solve(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream=None, out=None,
-          precision: int | None = None, algo: int | None = None, work_counters=None) -> dict:
+          precision: int | None = None, algo: int | None = None, work_counters=None, trace: bool = False) -> dict:
     """Solve scenarios held in CUDA tensors; returns CUDA output tensors
-    (enqueued on `stream`, default torch's current stream)."""
+    (enqueued on `stream`, default torch's current stream).  trace=True adds
+    out["trace"]: the [n, K] int32 row choices S of gamma* (debug export)."""
     import torch
-    n, K = I.shape
+    n, K = _check_inputs(I, p, g, alpha, coeffs, I.device)
     dev = I.device
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)
     o = out if out is not None else _alloc_out(torch, n, K, dev, want_w)
+    if trace and o.get("trace") is None:
+        o["trace"] = torch.empty((n, K), dtype=torch.int32, device=dev)
+    if params.get("batching_policy", 0) == BATCH_PER_BATCH_GAMMA and o.get("batch_gamma") is None:
+        o["batch_gamma"] = torch.empty((n, K), dtype=torch.int32, device=dev)
+    for k, v in o.items():
+        if hasattr(v, "is_contiguous"):
+            _check(f"out[{k}]", v, v.dtype, v.shape, dev)
     sdedge_solve_batch(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end"],
-                       o["order"], o["w"], o["status"], work_counters)
+                       o["order"], o["w"], o["status"], work_counters, o.get("trace"), o.get("batch_gamma"))
     return o
 
 
@@ -235,7 +321,7 @@ def solve_host(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, s
     """Solve scenarios held in (pinned) host tensors through the host entry
     point; the copies run on `stream` (caller synchronises before reading)."""
     import torch
-    n, K = I.shape
+    n, K = _check_inputs(I, p, g, alpha, coeffs, "host")
     if stream is None:
         stream = torch.cuda.current_stream()
     P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)

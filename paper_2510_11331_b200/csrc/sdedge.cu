@@ -21,6 +21,7 @@
 // plus the hoisted verify sum (N-1) Av + Bv (N-1)N/2 and the n = 1 term.
 #include "sdedge.h"
 
+#include <cuda.h>          // driver-API types only (entry points are fetched at run time: no -lcuda)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -28,6 +29,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <mutex>
 
 namespace {
 
@@ -70,6 +72,7 @@ struct Consts {
     int rows_in_smem;                    // DP row state in shared (1) or global (0) memory
     long long pool_cap;                  // envelope segments per warp slot
     long long rows_stride;               // bytes of one warp's global row state
+    long long ybuf_stride;               // doubles of one CTA's per-batch-gamma rows, (K+1) x 2 x O_max
 };
 
 struct Inputs {
@@ -89,6 +92,8 @@ struct Outputs {
     double* w;
     int32_t* status;
     unsigned long long* work;   // [5] or null: candidates, candidate x segments, candidate-steps, rows, full evals
+    int32_t* trace;             // [n*K] or null: S vector of gamma* (row choices, the step-trace export)
+    int32_t* bgam;              // [n*K] or null: gamma of each batch m < M
 };
 
 // Work actually evaluated by one lane (reduced per CTA, flushed once at exit).
@@ -121,6 +126,7 @@ struct Work {
     long long* ovf_list;           // [n]
     unsigned char* rows;           // global row state (when not in smem)
     unsigned char* pool;           // envelope segment pools, one per warp slot
+    double* ybuf;                  // per-batch-gamma DP rows, one block of ybuf_stride doubles per CTA
 };
 
 // DP row state of one warp (SoA of pairs, generic pointers: smem or global).
@@ -180,6 +186,13 @@ __device__ inline Pool<R> carve_pool(unsigned char* base, long long cap)
 }
 
 // ------------------------------------------------------------ small helpers
+constexpr int kWarpsFwd = SDEDGE_WARPS;
+// CTA-wide barrier (a warp barrier when the CTA is one warp: orders shared memory too)
+__device__ inline void block_sync()
+{
+    if (kWarpsFwd == 1) __syncwarp();
+    else __syncthreads();
+}
 template <typename R> __device__ inline R rmax(R a, R b) { return a > b ? a : b; }
 template <typename R> __device__ inline R kinf();
 template <> __device__ inline double kinf<double>() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -398,17 +411,45 @@ __device__ inline double expected_tokens(double alpha, int gamma)
     return __ddiv_rn(__dsub_rn(1.0, A), __dsub_rn(1.0, alpha));
 }
 
+// The per-(scenario, gamma) stage-time constants (D1) for N = ceil(O_max / L) steps.
+__device__ inline DPConst make_dpconst(const Consts& C, int gamma, double L, int N, double c1d, double c2d,
+                                       double c1v, double c2v)
+{
+    DPConst D;
+    const int Mx = N - 1;                                        // n >= 2 <-> m = n-1 in [1, Mx]
+    D.g = gamma;
+    D.tri = D.g * (D.g - 1.0) * 0.5;                             // sum_{i=1}^{gamma} (i-1)
+    D.kd = c1d * (4.0 * C.Jd * (double)C.hd);
+    D.kv = c1v * (4.0 * C.Jv * (double)C.hv);
+    D.hd2 = 2.0 * C.hd + C.h2d;
+    D.hv2 = 2.0 * C.hv + C.h2v;
+    D.bdc = D.kd * D.g * L;
+    D.bvc = D.kv * (1.0 + D.g) * L;
+    D.c2dg = D.g * c2d;
+    D.c2vv = c2v + C.dl;
+    D.Mx = Mx;
+    D.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
+    return D;
+}
+
 // ------------------------------------------------------------ shared layout
 struct Smem {
     int* I;        // [K] original lengths
     int* Is;       // [K] sorted lengths
     int* ord;      // [K] sorted pos -> task
+    unsigned long long* key;  // [sort_len(K)] bitonic sort keys (biased I_k << 32 | k)
+    double* glb;   // [ng] pre-DP lower bound of T_inf(gamma), in gamma-index order
+    int* gord;     // [ng] gamma indices in the order the warps take them (most promising first)
+    double* pI;    // [K+1] prefix sums of the sorted I (exact integers), pI[0] = 0
+    double* pI2;   // [K+1] prefix sums of the sorted I^2
+    int* nq;       // [ng] N_gamma (per-batch-gamma policy)
+    DPConst* dq;   // [ng] stage-time constants per gamma (per-batch-gamma policy)
     short* jlo;    // [K] first feasible j of row i (memory window), > i if none
     short* jf;     // [K] fixed-plan policies: start j of the batch ending at row i, 0 if none
     short* jw;     // [kWarps][K] heuristic batching: the plan under evaluation
     double* tinf;  // [ng]
-    double* red;   // [2 * kWarps]
-    int* ctl;      // [0] gamma queue, [2] M, [3] bad flag
+    double* red;   // [5 * kWarps] per-warp partials: T_com, sum I/s, sum I, sum I^2, min single-batch T_inf
+    int* ctl;      // [0] gamma queue, [2] M, [3] bad flag, [4] gamma* index
     long long* sid;
     unsigned char* rows; // [kWarps] row states when rows_in_smem
 };
@@ -426,14 +467,28 @@ __host__ __device__ inline size_t tile_bytes()
            2 * (size_t)kTileCh * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
 }
 
+// bitonic sort length: the next power of two >= K
+__host__ __device__ inline int sort_len(int K)
+{
+    int p = 2;
+    while (p < K) p <<= 1;
+    return p;
+}
+
 template <typename R, int G>
 __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile)
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
+    b = (b + 15) & ~(size_t)15;
+    b += (size_t)sort_len(K) * sizeof(unsigned long long);
+    b += (size_t)ng * (sizeof(double) + 2 * sizeof(int));
+    b = (b + 15) & ~(size_t)15;
+    b += (size_t)ng * sizeof(DPConst);
+    b += 2 * (size_t)(K + 1) * sizeof(double);
     b += (size_t)(2 + kWarps) * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
-    b += (size_t)ng * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
+    b += (size_t)ng * sizeof(double) + 5 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
     if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K);
     if (tile) b += (size_t)kWarps * G * tile_bytes<R, G>();
@@ -447,12 +502,21 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     s.I = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.Is = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
     s.ord = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
+    b = (b + 15) & ~(size_t)15;
+    s.key = reinterpret_cast<unsigned long long*>(base + b); b += (size_t)sort_len(K) * sizeof(unsigned long long);
+    s.glb = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
+    s.gord = reinterpret_cast<int*>(base + b); b += (size_t)ng * sizeof(int);
+    s.nq = reinterpret_cast<int*>(base + b); b += (size_t)ng * sizeof(int);
+    b = (b + 15) & ~(size_t)15;
+    s.dq = reinterpret_cast<DPConst*>(base + b); b += (size_t)ng * sizeof(DPConst);
+    s.pI = reinterpret_cast<double*>(base + b); b += (size_t)(K + 1) * sizeof(double);
+    s.pI2 = reinterpret_cast<double*>(base + b); b += (size_t)(K + 1) * sizeof(double);
     s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jf = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jw = reinterpret_cast<short*>(base + b); b += (size_t)kWarps * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
-    s.red = reinterpret_cast<double*>(base + b); b += 2 * kWarps * sizeof(double);
+    s.red = reinterpret_cast<double*>(base + b); b += 5 * kWarps * sizeof(double);
     s.sid = reinterpret_cast<long long*>(base + b); b += 2 * sizeof(long long);
     s.ctl = reinterpret_cast<int*>(base + b); b += 8 * sizeof(int);
     b = (b + 15) & ~(size_t)15;
@@ -613,19 +677,7 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     const double L = expected_tokens(alpha, gamma);
     const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
     const int Mx = N - 1;                                        // n >= 2 <-> m = n-1 in [1, Mx]
-    DPConst D;
-    D.g = gamma;
-    D.tri = D.g * (D.g - 1.0) * 0.5;                             // sum_{i=1}^{gamma} (i-1)
-    D.kd = c1d * (4.0 * C.Jd * (double)C.hd);
-    D.kv = c1v * (4.0 * C.Jv * (double)C.hv);
-    D.hd2 = 2.0 * C.hd + C.h2d;
-    D.hv2 = 2.0 * C.hv + C.h2v;
-    D.bdc = D.kd * D.g * L;
-    D.bvc = D.kv * (1.0 + D.g) * L;
-    D.c2dg = D.g * c2d;
-    D.c2vv = c2v + C.dl;
-    D.Mx = Mx;
-    D.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
+    const DPConst D = make_dpconst(C, gamma, L, N, c1d, c2d, c1v, c2v);
     unsigned n_cand = 0, n_seg = 0;
 
     if (gl == 0) {                                               // row 0 == 0 (reading A3)
@@ -648,7 +700,10 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
         int jhi = i;
         if (jf) {                            // fixed plan: only the batch ending at i (if any)
             const int jfi = jf[i - 1];
-            if (jfi == 0) continue;
+            if (jfi == 0) {                  // not a batch end: no choice at this row (trace 0)
+                if (S && gl == 0) S[i - 1] = 0;
+                continue;
+            }
             if (jfi < jlo) { T_last = dinf(); break; }
             jlo = jhi = jfi;
         }
@@ -786,6 +841,91 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
     if (__ballot_sync(0xffffffffu, ovf_any) & gmask) { *overflow = true; T_last = dinf(); }
     work_flush(wc, active, n_cand, n_seg, n_cand, (unsigned long long)n_cand * (unsigned long long)N,
                gl == 0 ? (unsigned)rows_done : 0u);
+    return T_last;
+}
+
+// ------------------------------------------------------------ per-batch gamma
+// An EXTENSION (the paper fixes one l: P:555): Algorithm 1 over candidates (j, gamma),
+// each batch with its own L, N_gamma; at step n only the batches with N_gamma >= n run
+// (eq:latency_infer_batch's active set), so a finished batch passes the state through:
+// max{Upsilon0 + 0, Upsilon1} + 0 = Upsilon1.  Dense, one warp, fp64: the Upsilon rows (n = 1..Nmax,
+// Nmax = max N_gamma) live in a global workspace (row p: Y0[Nmax] then Y1[Nmax]); lanes take steps n,
+// every (j, gamma) candidate is a lane sum + butterfly.  Ties: largest j, then smallest gamma (NB1).
+__device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, short* S, short* Gm, WorkCount& wc)
+{
+    const int lane = threadIdx.x & 31, K = C.K, ng = C.ng;
+    const size_t rs = 2 * (size_t)Nmax;
+    for (int n = lane; n < Nmax; n += 32) { Y[n] = 0.0; Y[Nmax + n] = 0.0; }   // row 0 == 0 (reading A3)
+    __syncwarp();
+    unsigned n_cand = 0, rows = 0;
+    unsigned long long n_steps = 0;
+    double T_last = 0.0;
+    for (int i = 1; i <= K; ++i) {
+        const int jlo = sm.jlo[i - 1];
+        if (jlo > i) { T_last = dinf(); break; }
+        const int I = sm.Is[i - 1];
+        double best = dinf();
+        int bj = -1, bq = -1;
+        for (int j = jlo; j <= i; ++j) {
+            const double b = (double)(i - j + 1);
+            const double* y0p = Y + (size_t)(j - 1) * rs;
+            const double* y1p = y0p + Nmax;
+            for (int q = 0; q < ng; ++q) {
+                const DPConst& D = sm.dq[q];
+                const RowCoef rc = row_coef(D, I);
+                const int Nq = sm.nq[q];
+                const double td1 = fma(b, rc.td1, D.c2dg), tv1 = fma(b, rc.tv1, D.c2vv);
+                const double ad = fma(b, rc.ad, D.c2dg), av = fma(b, rc.av, D.c2vv);
+                const double sd = b * D.bdc, sv = b * D.bvc;
+                double acc = 0.0;
+                for (int n = 1 + lane; n <= Nmax; n += 32) {
+                    const double y1 = y1p[n - 1];
+                    if (n <= Nq) {
+                        const double x = (double)(n - 1);
+                        const double td = n == 1 ? td1 : fma(sd, x, ad), tv = n == 1 ? tv1 : fma(sv, x, av);
+                        acc += rmax(y0p[n - 1] + td, y1) + tv;      // eq:t_ij1 (reading A1)
+                    } else {
+                        acc += y1;                                  // batch finished: no stage time
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (acc < best || (acc == best && j > bj)) { best = acc; bj = j; bq = q; }   // NB1
+            }
+            n_cand += (unsigned)ng;
+            n_steps += (unsigned long long)ng * (unsigned long long)Nmax;
+        }
+        if (bj < 0) { T_last = dinf(); break; }
+        {   // eq:tt1 / eq:tt2 with (j*, gamma*)
+            const DPConst& D = sm.dq[bq];
+            const RowCoef rc = row_coef(D, I);
+            const int Nq = sm.nq[bq];
+            const double b = (double)(i - bj + 1);
+            const double td1 = fma(b, rc.td1, D.c2dg), tv1 = fma(b, rc.tv1, D.c2vv);
+            const double ad = fma(b, rc.ad, D.c2dg), av = fma(b, rc.av, D.c2vv);
+            const double sd = b * D.bdc, sv = b * D.bvc;
+            const double* y0p = Y + (size_t)(bj - 1) * rs;
+            double* o0 = Y + (size_t)i * rs;
+            for (int n = 1 + lane; n <= Nmax; n += 32) {
+                double y0 = y0p[n - 1], y1 = y0p[Nmax + n - 1];
+                if (n <= Nq) {
+                    const double x = (double)(n - 1);
+                    y0 += n == 1 ? td1 : fma(sd, x, ad);
+                    y1 = rmax(y0, y1) + (n == 1 ? tv1 : fma(sv, x, av));
+                }
+                o0[n - 1] = y0;
+                o0[Nmax + n - 1] = y1;
+            }
+        }
+        if (lane == 0) {
+            S[i - 1] = (short)bj;
+            Gm[i - 1] = (short)(C.gmin + bq);
+        }
+        __syncwarp();
+        ++rows;
+        T_last = best;
+    }
+    work_flush(wc, true, n_cand, 0u, n_cand, n_steps, lane == 0 ? rows : 0u);
     return T_last;
 }
 
@@ -1093,7 +1233,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                                  unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
                                  DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
                                  double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
-                                 const double* best_s)
+                                 const double* best_s, double lbv)
 {
     constexpr int GL = 32 / G;
     const int lane = threadIdx.x & 31;
@@ -1103,20 +1243,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     const double L = expected_tokens(alpha, gamma);
     const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
     const int Mx = N - 1;
-    DPConst Dl;
-    DPConst& D0 = Dl;
-    D0.g = gamma;
-    D0.tri = D0.g * (D0.g - 1.0) * 0.5;
-    D0.kd = c1d * (4.0 * C.Jd * (double)C.hd);
-    D0.kv = c1v * (4.0 * C.Jv * (double)C.hv);
-    D0.hd2 = 2.0 * C.hd + C.h2d;
-    D0.hv2 = 2.0 * C.hv + C.h2v;
-    D0.bdc = D0.kd * D0.g * L;
-    D0.bvc = D0.kv * (1.0 + D0.g) * L;
-    D0.c2dg = D0.g * c2d;
-    D0.c2vv = c2v + C.dl;
-    D0.Mx = Mx;
-    D0.sumM = (double)Mx * (double)(Mx + 1) * 0.5;
+    const DPConst Dl = make_dpconst(C, gamma, L, N, c1d, c2d, c1v, c2v);
     // the per-(scenario, gamma) constants live in shared memory: they are read
     // once per tile, and keeping all twelve in registers spills the phase-A loop
     if (gl == 0) *Ds = Dl;
@@ -1143,11 +1270,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         // sum_m (b_m vsl(I_m) + vc) >= sum_k vsl(I_k) + vc, since vsl grows with I and
         // each task pays at least its own length's slope.  A gamma whose
         // bound already exceeds the best finished T_inf never starts.
-        double lbv = 0.0;
-        for (int r = gl; r < K; r += GL) lbv += row_coef(D, sm.Is[r]).vsl;
-#pragma unroll
-        for (int o = 1; o < GL; o <<= 1) lbv += __shfl_xor_sync(0xffffffffu, lbv, o);
-        lbv += D.c2vv * (D.Mx + 1.0);
+        // (lbv is computed per scenario in O(1) from sum I and sum I^2: solve_kernel's prologue)
         const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;       // covers the rounding of either DP
         aborted |= lbv * (1.0 - mg) > *best_s * (1.0 + mg);
         if (__all_sync(0xffffffffu, aborted)) {
@@ -1419,10 +1542,21 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         // its padded length cannot grow, every stage time can only fall), so once
         // T*(i0+GL-1) exceeds the best T_inf of an already finished gamma, this gamma
         // cannot win or tie.  Margins cover the rounding of both DPs.
+        // Stronger: Upsilon[i+1,0,0] >= Upsilon[i,0,0] + vsl(I_{i+1}) -- every
+        // candidate of row i+1 either extends a candidate of row i by task i+1 (its verify
+        // stage grows by at least that task's own verify time, every other stage time can only
+        // grow) or appends a new batch after row i's state -- so T_inf >= Upsilon[i,0,0] + the
+        // remaining tasks' own verify work sum_{k>i} vsl(I_k), quadratic in I_k: O(1) from the
+        // suffix sums of I and I^2.
         if (best_s && rend == GL) {
+            const int il = i0 + GL - 1;                          // the tile's last row
             const R kl = __shfl_sync(0xffffffffu, t_row, (lane - gl) + GL - 1);
             const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
-            aborted |= (double)kl * (1.0 - mg) > *best_s * (1.0 + mg);
+            const double S1 = sm.pI[K] - sm.pI[il], S2 = sm.pI2[K] - sm.pI2[il], cnt = (double)(K - il);
+            const double c = D.hv2 + D.g;
+            const double rest = D.kv * (S2 + (D.g + c) * S1 + cnt * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + cnt * c) +
+                                cnt * D.bvc * D.sumM;
+            aborted |= ((double)kl + rest) * (1.0 - mg) > *best_s * (1.0 + mg);
             if (__all_sync(0xffffffffu, aborted)) break;
         }
 #endif
@@ -1485,7 +1619,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                                          (size_t)(wu * G) * tb_stride) + (unsigned)(GL * sizeof(RowRec<R>)) : 0u;
     const unsigned char* rw0 = ws.rows + (size_t)((long long)blockIdx.x * kWarps + wu) * G * C.rows_stride;
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
-    short* Scta = ws.S + (size_t)blockIdx.x * ng * K;   // this CTA's S vectors (global, L2 resident)
+    short* Scta = ws.S + (size_t)blockIdx.x * (ng + 1) * K;   // this CTA's S vectors (+1: per-batch gammas)
     __shared__ bool s_ovf;
     __shared__ double s_best;                // best T_inf of the finished gammas of this scenario
     __shared__ unsigned long long s_work[5];
@@ -1519,16 +1653,59 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (Ik < 1 || !(pk > 0.0) || !(gk > 0.0) || !isfinite(pk) || !isfinite(gk)) bad = 1;
         }
         bad = __syncthreads_or(bad);
-        // ---- stable ascending sort by I_k (reading A13): rank = #{smaller or equal-and-earlier}
-        for (int k = tid; k < K; k += kThreads) {
-            const int Ik = sm.I[k];
-            int r = 0;
-            for (int q = 0; q < K; ++q) {
-                const int Iq = sm.I[q];
-                r += (Iq < Ik) || (Iq == Ik && q < k);
+        // ---- stable ascending sort by I_k (reading A13): bitonic sort of the unique keys
+        // (I_k biased to unsigned) << 32 | k, padded to a power of two with ~0 -- O(K log^2 K / threads)
+        {
+            const int P2 = sort_len(K);
+            for (int k = tid; k < P2; k += kThreads)
+                sm.key[k] = k < K ? ((unsigned long long)((unsigned)sm.I[k] ^ 0x80000000u) << 32) | (unsigned)k
+                                  : ~0ULL;
+            block_sync();
+            for (int sz = 2; sz <= P2; sz <<= 1)
+                for (int st = sz >> 1; st > 0; st >>= 1) {
+                    for (int t = tid; t < (P2 >> 1); t += kThreads) {
+                        const int a = ((t & ~(st - 1)) << 1) | (t & (st - 1)), b = a + st;
+                        const unsigned long long ka = sm.key[a], kb = sm.key[b];
+                        if ((ka > kb) == ((a & sz) == 0)) { sm.key[a] = kb; sm.key[b] = ka; }
+                    }
+                    block_sync();
+                }
+            for (int r = tid; r < K; r += kThreads) {
+                const int k = (int)(unsigned)(sm.key[r] & 0xffffffffULL);
+                sm.ord[r] = k;
+                sm.Is[r] = sm.I[k];
             }
-            sm.ord[r] = k;
-            sm.Is[r] = Ik;
+        }
+        __syncthreads();
+        // prefix sums of the sorted I and I^2 (the suffix verify-work bound):
+        // each thread a contiguous chunk, then an exclusive scan of the chunk sums
+        {
+            const int ch = (K + kThreads - 1) / kThreads, a0 = min(K, tid * ch), a1 = min(K, a0 + ch);
+            double c1 = 0.0, c2 = 0.0;
+            for (int r = a0; r < a1; ++r) { const double x = sm.Is[r]; c1 += x; c2 += x * x; }
+            if (kWarps == 1) {
+                double e1 = c1, e2 = c2;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double u1 = __shfl_up_sync(0xffffffffu, e1, o), u2 = __shfl_up_sync(0xffffffffu, e2, o);
+                    if (lane >= o) { e1 += u1; e2 += u2; }
+                }
+                e1 -= c1; e2 -= c2;                                  // exclusive
+                if (tid == 0) { sm.pI[0] = 0.0; sm.pI2[0] = 0.0; }
+                for (int r = a0; r < a1; ++r) {
+                    const double x = sm.Is[r];
+                    e1 += x; e2 += x * x;
+                    sm.pI[r + 1] = e1; sm.pI2[r + 1] = e2;
+                }
+            } else if (tid == 0) {
+                double e1 = 0.0, e2 = 0.0;
+                sm.pI[0] = 0.0; sm.pI2[0] = 0.0;
+                for (int r = 0; r < K; ++r) {
+                    const double x = sm.Is[r];
+                    e1 += x; e2 += x * x;
+                    sm.pI[r + 1] = e1; sm.pI2[r + 1] = e2;
+                }
+            }
         }
         __syncthreads();
         // ---- memory window per sorted row (gamma-independent): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
@@ -1541,9 +1718,12 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2), or the
         // uniform baseline w_k = 1/K with T_com = max_k T_k,com (eq:ul_latency)
         const bool uniform = C.bw_policy == SDEDGE_BW_UNIFORM;
-        double tc = 0.0, q = 0.0;
+        double tc = 0.0, q = 0.0, s1 = 0.0, s2 = 0.0;   // s1, s2: sum I_k, sum I_k^2 (exact integers)
         if (!bad)
             for (int k = tid; k < K; k += kThreads) {
+                const double Ikd = (double)sm.I[k];
+                s1 += Ikd;
+                s2 += Ikd * Ikd;
                 const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
                 if (uniform) {
                     const double r = (1.0 / K) * C.Bw * sk;
@@ -1557,8 +1737,13 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             const double ot = __shfl_xor_sync(0xffffffffu, tc, o);
             tc = uniform ? fmax(tc, ot) : tc + ot;
             q += __shfl_xor_sync(0xffffffffu, q, o);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
         }
-        if (lane == 0) { sm.red[warp] = tc; sm.red[kWarps + warp] = q; }
+        if (lane == 0) {
+            sm.red[warp] = tc; sm.red[kWarps + warp] = q;
+            sm.red[2 * kWarps + warp] = s1; sm.red[3 * kWarps + warp] = s2;
+        }
         // ---- fixed-plan baselines (gamma-independent): start of the batch ending at each row
         if (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX) {
             int b = 1;
@@ -1594,16 +1779,77 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         // stage times non-decreasing in b and I (non-negative coefficients): the row
         // optimum is then monotone in the row, which the gamma-level pruning needs
         const bool mono = s_par[1] >= 0.0 && s_par[2] >= 0.0 && s_par[3] >= 0.0 && s_par[4] >= 0.0 && C.dl >= 0.0;
-        // ---- P3: each warp pulls gamma values and runs Algorithm 1 (P:755-767)
+        // ---- per-gamma prologue, one gamma per thread:
+        //  * the verify-work lower bound T_inf(gamma) >= sum_k vsl(I_k) + vc, in O(1): vsl is a
+        //    quadratic in I, so the sum needs only sum I and sum I^2;
+        //  * the closed-form latency of the single batch of all K tasks -- row K's j = 1 candidate,
+        //    so T_inf(gamma) <= it; its minimum over gamma seeds s_best, the best
+        //    finished T_inf, before any DP runs;
+        //  * the order in which the warps take the gammas: ascending lower bound (the most
+        //    promising first, so s_best tightens early).  The result does not depend on the order:
+        //    gamma* is the smallest argmin over the stored T_inf (reading A7).
         if (!bad && !bad_alpha) {
+            double S1 = 0.0, S2 = 0.0;
+            for (int w = 0; w < kWarps; ++w) { S1 += sm.red[2 * kWarps + w]; S2 += sm.red[3 * kWarps + w]; }
+            const double Kd = (double)K;
+            const bool one_fits = sm.jlo[K - 1] == 1;     // a batch of all K tasks fits the memory
+            double one_min = dinf();
+            for (int gi = tid; gi < ng; gi += kThreads) {
+                const int gamma = C.gmin + gi;
+                const double L = expected_tokens(s_par[0], gamma);
+                const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));
+                const DPConst D = make_dpconst(C, gamma, L, N, s_par[1], s_par[2], s_par[3], s_par[4]);
+                sm.dq[gi] = D;
+                sm.nq[gi] = N;
+                const double c = D.hv2 + D.g;
+                sm.glb[gi] = D.kv * (S2 + (D.g + c) * S1 + Kd * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + Kd * c) +
+                             Kd * D.bvc * D.sumM + D.c2vv * (D.Mx + 1.0);
+                if (one_fits) {
+                    const RowCoef rc = row_coef(D, sm.Is[K - 1]);
+                    one_min = fmin(one_min, Kd * (rc.td1 + rc.tv1 + D.Mx * (rc.ad + rc.av) + D.sumM * (D.bdc + D.bvc)) +
+                                                (D.c2dg + D.c2vv) * (D.Mx + 1.0));
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) one_min = fmin(one_min, __shfl_xor_sync(0xffffffffu, one_min, o));
+            if (lane == 0) sm.red[4 * kWarps + warp] = one_min;
+            __syncthreads();
+            for (int gi = tid; gi < ng; gi += kThreads) {
+                const double v = sm.glb[gi];
+                int r = 0;
+                for (int q2 = 0; q2 < ng; ++q2) {
+                    const double u = sm.glb[q2];
+                    r += (u < v) || (u == v && q2 < gi) || (v != v && (u == u || q2 < gi));   // NaN bounds last
+                }
+                sm.gord[r] = gi;
+            }
+            if (tid == 0) {
+                double m = dinf();
+                for (int w = 0; w < kWarps; ++w) m = fmin(m, sm.red[4 * kWarps + w]);
+                s_best = m;
+            }
+            __syncthreads();
+        }
+        // ---- P3: each warp pulls gamma values and runs Algorithm 1 (P:755-767)
+        const bool pbg = C.batch_policy == SDEDGE_BATCH_PER_BATCH_GAMMA;
+        if (pbg) {
+            if constexpr (sizeof(R) == 8 && G == 1 && !TILE) {   // per-batch gamma: one dense DP (warp 0)
+                if (!bad && !bad_alpha && warp == 0) {
+                    int Nmax = 0;
+                    for (int q = lane; q < ng; q += 32) Nmax = max(Nmax, sm.nq[q]);
+                    Nmax = __reduce_max_sync(0xffffffffu, Nmax);
+                    const double t = dp_pbg(C, sm, ws.ybuf + (size_t)blockIdx.x * C.ybuf_stride, Nmax, Scta,
+                                            Scta + (size_t)ng * K, wc);
+                    if (lane == 0) sm.tinf[0] = t;
+                }
+            }
+        } else if (!bad && !bad_alpha) {
             for (;;) {
                 int gi0 = 0;
                 if (lane == 0) gi0 = atomicAdd(&sm.ctl[0], G);
                 gi0 = __shfl_sync(0xffffffffu, gi0, 0);
                 if (gi0 >= ng) break;
-                int gi = gi0 + grp;
-                const bool active = gi < ng;       // an idle group repeats gi0 without writing
-                if (!active) gi = gi0;
+                const bool active = gi0 + grp < ng;  // an idle group repeats gi0 without writing
+                const int gi = sm.gord[active ? gi0 + grp : gi0];   // queue position -> gamma index
                 bool ovf = false;
                 short* Sg = active ? Scta + (size_t)gi * K : nullptr;
                 const short* jf = (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX)
@@ -1616,7 +1862,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
                                              C.rows_stride, dpc, C.gmin + gi, SDEDGE_SCEN_ARGS,
                                              Sg, &ovf, wc, &s_top[warp * G + grp], active,
-                                             (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr);
+                                             (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr, sm.glb[gi]);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
                     // 2, 3, ... in sorted order until the pipelined latency stops improving
@@ -1645,8 +1891,17 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
                                              &s_top[warp * G + grp], active, jw);
                 } else {
-                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
-                                             &s_top[warp * G + grp], active, kBase ? jf : nullptr);
+                    // exact gamma-level pruning before the first row, for the
+                    // proposed policy: a gamma whose lower bound exceeds the best finished (or
+                    // seeded) T_inf cannot win or tie; the call is skipped when every group's can't
+                    bool skip = false;
+                    if (SDEDGE_GAMMA_ABORT && mono && C.batch_policy == SDEDGE_BATCH_PROPOSED) {
+                        const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
+                        skip = __all_sync(0xffffffffu, !active || sm.glb[gi] * (1.0 - mg) > s_best * (1.0 + mg));
+                    }
+                    t = skip ? dinf()
+                             : dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
+                                                    &s_top[warp * G + grp], active, kBase ? jf : nullptr);
                 }
                 if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
@@ -1685,18 +1940,23 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (bad) st = 3;
             else if (bad_alpha) st = 2;
             else if (s_ovf) st = 5;          // cannot happen with the worst-case pool
-            else {
+            else if (pbg) {
+                best = sm.tinf[0];
+                gbest = best < dinf() ? 0 : -1;
+                if (gbest < 0) st = 1;
+            } else {
                 for (int gi = 0; gi < ng; ++gi)
                     if (sm.tinf[gi] < best) { best = sm.tinf[gi]; gbest = gi; }
                 if (gbest < 0) st = 1;
             }
             double* lat = out.lat + 3 * s;
+            sm.ctl[4] = gbest;
             if (st == 0) {
                 const short* S = Scta + (size_t)gbest * K;
                 int i = K;
                 while (i > 0) { sm.I[M++] = i; i = S[i - 1] - 1; }   // reuse sm.I as a stack
                 lat[0] = Tcom + best; lat[1] = Tcom; lat[2] = best;
-                out.gamma[s] = C.gmin + gbest;
+                out.gamma[s] = pbg ? (int)Scta[(size_t)ng * K + K - 1] : C.gmin + gbest;   // pbg: the last batch's
             } else {
                 const double nan = dnan();
                 lat[0] = st == 1 ? dinf() : nan;
@@ -1714,6 +1974,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         for (int k = tid; k < K; k += kThreads) {
             out.order[s * K + k] = sm.ord[k];
             out.bend[s * K + k] = k < M ? sm.I[M - 1 - k] : 0;
+        }
+        if (out.bgam)                        // each batch's gamma (gamma* for all unless per-batch)
+            for (int k = tid; k < K; k += kThreads)
+                out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + sm.I[M - 1 - k] - 1]
+                                                       : C.gmin + sm.ctl[4];
+        if (out.trace) {                     // S vector of gamma* (row choices; 0 unless status 0)
+            const short* S = Scta + (size_t)max(sm.ctl[4], 0) * K;
+            for (int k = tid; k < K; k += kThreads) out.trace[s * K + k] = M > 0 ? (int32_t)S[k] : 0;
         }
         if (out.w)
             for (int k = tid; k < K; k += kThreads) {
@@ -1754,9 +2022,25 @@ actual_kernel(const Consts C, const Inputs in, const int32_t* __restrict__ O, co
     for (long long s = (long long)blockIdx.x * (blockDim.x >> 5) + warp; s < n; s += nw) {
         const int M = Mv[s];
         const int g = gam[s];
-        if (status[s] != 0 || M < 1 || M > K) {
+        if (status[s] != 0 || M < 1 || M > K || g < 0 || g > 64) {
             if (lane == 0) out[s] = dnan();
             continue;
+        }
+        {   // the plan is caller data: batch ends strictly increasing in [1, K] ending at K, order a
+            // permutation range -- anything else yields NaN instead of out-of-bounds reads
+            int badp = 0;
+            for (int m = lane; m < M; m += 32) {
+                const int e = bend[s * K + m], pv = m ? bend[s * K + m - 1] : 0;
+                badp |= e < 1 || e > K || e <= pv || (m == M - 1 && e != K);
+            }
+            for (int q = lane; q < K; q += 32) {
+                const int o = order[s * K + q];
+                badp |= o < 0 || o >= K;
+            }
+            if (__any_sync(0xffffffffu, badp)) {
+                if (lane == 0) out[s] = dnan();
+                continue;
+            }
         }
         const double alpha = in.alpha[s];
         double c1d = C.c1d, c2d = C.c2d, c1v = C.c1v, c2v = C.c2v;
@@ -2101,8 +2385,13 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
     if (p->flags & ~SDEDGE_FLAG_TINY_POOL) return fail(-1, "unknown flags");
     if (p->bandwidth_policy != SDEDGE_BW_OPTIMAL && p->bandwidth_policy != SDEDGE_BW_UNIFORM)
         return fail(-1, "unknown bandwidth_policy");
-    if (p->batching_policy < SDEDGE_BATCH_PROPOSED || p->batching_policy > SDEDGE_BATCH_HEURISTIC)
+    if (p->batching_policy < SDEDGE_BATCH_PROPOSED || p->batching_policy > SDEDGE_BATCH_PER_BATCH_GAMMA)
         return fail(-1, "unknown batching_policy");
+    if (p->batching_policy == SDEDGE_BATCH_PER_BATCH_GAMMA) {
+        if (p->precision != 0) return fail(-1, "per-batch gamma is fp64 only");
+        if (p->gamma_max - p->gamma_min + 1 > 32) return fail(-1, "per-batch gamma: at most 32 speculation lengths");
+        if ((long long)(p->K + 1) * 2 * p->O_max * 8 > (2LL << 30)) return fail(-1, "per-batch gamma: (K+1) O_max too large");
+    }
     if (p->batching_policy == SDEDGE_BATCH_STATIC && p->static_batch < 1) return fail(-1, "static_batch < 1");
     if (p->reserved != 0) return fail(-1, "reserved must be 0");
     if (!(p->downlink_s >= 0) || !std::isfinite(p->downlink_s)) return fail(-1, "downlink_s must be >= 0");
@@ -2123,17 +2412,39 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
         }                                                                       \
     } while (0)
 
-// Keep stream-ordered workspace cached in the device's default pool between
-// calls (the default release threshold of 0 returns it at every sync point).
-int keep_pool_cached(int dev)
+// Stream-ordered workspace comes from ONE library-private memory pool per device
+// (created on first use, release threshold "never", so the workspace stays cached
+// between calls); the device's default pool -- and every other allocator of the
+// caller's process -- is left untouched.
+int lib_pool(int dev, cudaMemPool_t* out)
 {
-    static thread_local int done_mask = 0;   // devices < 32 handled on this thread
-    if (dev < 32 && (done_mask >> dev & 1)) return 0;
-    cudaMemPool_t pool;
-    CU(cudaDeviceGetDefaultMemPool(&pool, dev));
-    unsigned long long thr = ~0ULL;
-    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    if (dev < 32) done_mask |= 1 << dev;
+    static std::mutex mu;
+    static cudaMemPool_t pools[256] = {};
+    if (dev < 0 || dev >= 256) return fail(-1, "device ordinal out of range");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pl = nullptr;
+        CU(cudaMemPoolCreate(&pl, &props));
+        unsigned long long thr = ~0ULL;
+        CU(cudaMemPoolSetAttribute(pl, cudaMemPoolAttrReleaseThreshold, &thr));
+        pools[dev] = pl;
+    }
+    *out = pools[dev];
+    return 0;
+}
+
+// cudaMallocAsync from the library pool of the current device
+int ws_alloc(void** ptr, size_t bytes, cudaStream_t st)
+{
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    cudaMemPool_t pl = nullptr;
+    if (int rc = lib_pool(dev, &pl)) return rc;
+    CU(cudaMallocFromPoolAsync(ptr, bytes, pl, st));
     return 0;
 }
 
@@ -2142,7 +2453,6 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
 {
     int dev = 0, nsm = 0, max_smem = 0;
     CU(cudaGetDevice(&dev));
-    if (int rc = keep_pool_cached(dev)) return rc;
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
 
@@ -2164,6 +2474,10 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_main, kThreads, sb));
     if (occ < 1) return fail(-1, "kernel does not fit on an SM");
     long long grid = (long long)nsm * occ;
+    const bool pbg = C.batch_policy == SDEDGE_BATCH_PER_BATCH_GAMMA;
+    // per-batch gamma: (K+1) Upsilon rows of 2 x Nmax doubles per CTA (Nmax <= O_max); <= 2 GiB in all
+    C.ybuf_stride = pbg ? (long long)(C.K + 1) * 2 * C.O_max : 0;
+    if (pbg) grid = std::max(1LL, std::min(grid, (2LL << 30) / (8 * C.ybuf_stride)));
     if (grid > n) grid = n;
 
     // typical envelopes have <= a few segments per row: 4 (K+1) + 64 extra
@@ -2171,20 +2485,22 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     // with the worst-case bound sum_i 2i = K(K+1) (D3).
     const long long cap_main = (flags & SDEDGE_FLAG_TINY_POOL) ? 8LL : (4LL * (C.K + 1) + 64 + 7) & ~7LL;
     const long long cap_big = ((long long)C.K * (C.K + 1) + 64 + 7) & ~7LL;
-    long long grid_big = std::max(1LL, std::min((long long)nsm,
+    long long grid_big = std::max(1LL, std::min(std::min((long long)nsm, std::max(n, 1LL)),
                                   (2LL << 30) / (long long)(kWarps * G * pool_bytes<R>(cap_big))));
+    if (pbg) grid_big = 1;                   // no envelopes: the second pass has nothing to do
     const long long slots = grid * kWarps * G, slots_big = grid_big * kWarps * G;
 
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
     const size_t o_next = take(2 * sizeof(unsigned long long) + sizeof(unsigned int));
-    const size_t o_S = take((size_t)std::max(grid, grid_big) * C.ng * C.K * sizeof(short));
+    const size_t o_S = take((size_t)std::max(grid, grid_big) * (C.ng + 1) * C.K * sizeof(short));
     const size_t o_list = take((size_t)n * sizeof(long long));
     const size_t o_rows = take(C.rows_in_smem ? 0 : (size_t)std::max(slots, slots_big) * C.rows_stride);
     const size_t o_pool = take((size_t)slots * pool_bytes<R>(cap_main));
-    const size_t o_pool_big = take((size_t)slots_big * pool_bytes<R>(cap_big));
+    const size_t o_pool_big = take(pbg ? 0 : (size_t)slots_big * pool_bytes<R>(cap_big));
+    const size_t o_ybuf = take((size_t)grid * C.ybuf_stride * sizeof(double));
     unsigned char* wsb = nullptr;
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&wsb), off, st));
+    if (int rc = ws_alloc(reinterpret_cast<void**>(&wsb), off, st)) return rc;
     CU(cudaMemsetAsync(wsb + o_next, 0, 2 * sizeof(unsigned long long) + sizeof(unsigned int), st));
 
     Work w;
@@ -2193,6 +2509,7 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     w.ovf_count = reinterpret_cast<unsigned int*>(wsb + o_next + 2 * sizeof(unsigned long long));
     w.ovf_list = reinterpret_cast<long long*>(wsb + o_list);
     w.rows = wsb + o_rows;
+    w.ybuf = reinterpret_cast<double*>(wsb + o_ybuf);
 
     int launches = 0;
     if (n > 0) {
@@ -2237,7 +2554,7 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     Consts C = make_consts(p);
     Inputs in{s->input_len, s->tx_power_w, s->gain, s->alpha, s->coeffs};
     Outputs out{lat, o->gamma, o->num_batches, o->batch_end, o->order, o->bw_share, o->status,
-                reinterpret_cast<unsigned long long*>(o->work_counters)};
+                reinterpret_cast<unsigned long long*>(o->work_counters), o->row_choice, o->batch_gamma};
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
     // envelope, proposed policy: small K -> G DPs per warp with row state in shared
     // memory; larger K -> the tiled DP (rows in global memory, a GL-row shared tile
@@ -2258,6 +2575,124 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     if (tiled) return launch_all<float, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 1>(C, in, out, n, st, f);
     if (G == 4) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 4, 0>(C, in, out, n, st, f);
     return launch_all<float, SDEDGE_ALGO_ENVELOPE, 2, 0>(C, in, out, n, st, f);
+}
+
+// ---- the host entry point's pipeline state (sdedge_solve_batch_host)
+constexpr int kHostStreams = 4;              // 0: H2D, 1-2: solves, 3: D2H
+constexpr int kHostMaxChunks = 16;
+
+struct HostPipe {
+    unsigned char* d = nullptr;
+    cudaStream_t ss[kHostStreams] = {};
+    cudaEvent_t ev0 = nullptr, evh[kHostMaxChunks] = {}, evc[kHostMaxChunks] = {}, evj[kHostStreams] = {};
+
+    // Join every internal stream into the caller's stream, free, destroy.  Runs on
+    // success and failure alike; returns the first error it meets (0 if none).
+    int finish(cudaStream_t st)
+    {
+        int rc = 0;
+        auto keep = [&](cudaError_t e, const char* what) {
+            if (e != cudaSuccess && rc == 0) {
+                snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+                rc = e == cudaErrorMemoryAllocation ? -3 : -2;
+            }
+        };
+        for (int q = 0; q < kHostStreams; ++q) {
+            if (!ss[q]) continue;
+            if (!evj[q]) keep(cudaEventCreateWithFlags(&evj[q], cudaEventDisableTiming), "cudaEventCreate");
+            if (evj[q]) {
+                keep(cudaEventRecord(evj[q], ss[q]), "cudaEventRecord(join)");
+                keep(cudaStreamWaitEvent(st, evj[q], 0), "cudaStreamWaitEvent(join)");
+            } else {
+                keep(cudaStreamSynchronize(ss[q]), "cudaStreamSynchronize");   // last resort: wait on the host
+            }
+        }
+        if (d) keep(cudaFreeAsync(d, st), "cudaFreeAsync");
+        for (int q = 0; q < kHostStreams; ++q)
+            if (ss[q]) keep(cudaStreamDestroy(ss[q]), "cudaStreamDestroy");   // released once their work drains
+        if (ev0) keep(cudaEventDestroy(ev0), "cudaEventDestroy");
+        for (int q = 0; q < kHostMaxChunks; ++q) {
+            if (evh[q]) keep(cudaEventDestroy(evh[q]), "cudaEventDestroy");
+            if (evc[q]) keep(cudaEventDestroy(evc[q]), "cudaEventDestroy");
+        }
+        for (int q = 0; q < kHostStreams; ++q)
+            if (evj[q]) keep(cudaEventDestroy(evj[q]), "cudaEventDestroy");
+        *this = HostPipe{};
+        return rc;
+    }
+};
+
+int host_pipeline(HostPipe& hp, const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
+                  sdedge_schedule* o, cudaStream_t st)
+{
+    const size_t K = (size_t)p->K, nn = (size_t)n;
+    const size_t bI = nn * K * 4, bD = nn * K * 8, bA = nn * 8, bC = s->coeffs ? nn * 32 : 0;
+    const size_t bLat = nn * 24, bS = nn * 4, bW = o->bw_share ? nn * K * 8 : 0;
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t q = off; off += (b + 255) & ~(size_t)255; return q; };
+    const size_t oI = take(bI), oP = take(bD), oG = take(bD), oA = take(bA), oC = take(bC);
+    const size_t oLat = take(bLat), oGm = take(bS), oM = take(bS), oBe = take(bI), oOr = take(bI),
+                 oW = take(bW), oSt = take(bS);
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    if (int rc2 = ws_alloc(reinterpret_cast<void**>(&hp.d), off, st)) return rc2;
+    unsigned char* d = hp.d;
+    for (int q = 0; q < kHostStreams; ++q) CU(cudaStreamCreateWithFlags(&hp.ss[q], cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&hp.ev0, cudaEventDisableTiming));
+    for (int q = 0; q < kHostMaxChunks; ++q) {
+        CU(cudaEventCreateWithFlags(&hp.evh[q], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&hp.evc[q], cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(hp.ev0, st));
+    for (int q = 0; q < kHostStreams; ++q) CU(cudaStreamWaitEvent(hp.ss[q], hp.ev0, 0));
+
+    const long long nch = std::max(1LL, std::min((long long)kHostMaxChunks, (long long)(n / 32768)));
+    const long long chunk = (n + nch - 1) / nch;
+    int launches = 0;
+    auto h2d = [&](size_t doff, const void* src, size_t row, long long a, long long m, cudaStream_t q) {
+        return cudaMemcpyAsync(d + doff + row * a, static_cast<const unsigned char*>(src) + row * a, row * m,
+                               cudaMemcpyHostToDevice, q);
+    };
+    auto d2h = [&](void* dst, size_t doff, size_t row, long long a, long long m, cudaStream_t q) {
+        return cudaMemcpyAsync(static_cast<unsigned char*>(dst) + row * a, d + doff + row * a, row * m,
+                               cudaMemcpyDeviceToHost, q);
+    };
+    for (long long c = 0; c < nch; ++c) {
+        const long long a = c * chunk, m = std::min(chunk, (long long)n - a);
+        if (m <= 0) break;
+        cudaStream_t q = hp.ss[0];
+        CU(h2d(oI, s->input_len, K * 4, a, m, q));
+        CU(h2d(oP, s->tx_power_w, K * 8, a, m, q));
+        CU(h2d(oG, s->gain, K * 8, a, m, q));
+        CU(h2d(oA, s->alpha, 8, a, m, q));
+        if (bC) CU(h2d(oC, s->coeffs, 32, a, m, q));
+        CU(cudaEventRecord(hp.evh[c], q));
+        q = hp.ss[1 + (c & 1)];
+        CU(cudaStreamWaitEvent(q, hp.evh[c], 0));
+        sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI) + a * K, reinterpret_cast<double*>(d + oP) + a * K,
+                            reinterpret_cast<double*>(d + oG) + a * K, reinterpret_cast<double*>(d + oA) + a,
+                            bC ? reinterpret_cast<double*>(d + oC) + a * 4 : nullptr};
+        sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm) + a, reinterpret_cast<int32_t*>(d + oM) + a,
+                             reinterpret_cast<int32_t*>(d + oBe) + a * K, reinterpret_cast<int32_t*>(d + oOr) + a * K,
+                             bW ? reinterpret_cast<double*>(d + oW) + a * K : nullptr,
+                             reinterpret_cast<int32_t*>(d + oSt) + a, nullptr, nullptr, nullptr};
+        sdedge_params pc = *p;
+        pc.stream = q;
+        if (int rc = solve_device(&ds, m, &pc, reinterpret_cast<double*>(d + oLat) + 3 * a, &dsch)) return rc;
+        launches += g_launches;
+        CU(cudaEventRecord(hp.evc[c], q));
+        q = hp.ss[3];
+        CU(cudaStreamWaitEvent(q, hp.evc[c], 0));
+        CU(d2h(out_latency, oLat, 24, a, m, q));
+        CU(d2h(o->gamma, oGm, 4, a, m, q));
+        CU(d2h(o->num_batches, oM, 4, a, m, q));
+        CU(d2h(o->batch_end, oBe, K * 4, a, m, q));
+        CU(d2h(o->order, oOr, K * 4, a, m, q));
+        if (bW) CU(d2h(o->bw_share, oW, K * 8, a, m, q));
+        CU(d2h(o->status, oSt, 4, a, m, q));
+    }
+    g_launches = launches;
+    return 0;
 }
 
 }  // namespace
@@ -2290,100 +2725,21 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     // (solve c after H2D c, D2H c after solve c).  So both copy directions run
     // back to back while chunks are solved, and the solves of neighbouring chunks
     // can overlap each other's tail.  The caller's stream is joined at the end
-    // (one cudaMemcpyAsync per array and chunk).
+    // (one cudaMemcpyAsync per array and chunk).  On ANY failure after the first
+    // allocation the same cleanup runs: the caller's stream waits for everything
+    // already queued on the internal streams (so the caller's documented stream
+    // sync still covers every DMA touching its buffers), then the device buffer is
+    // freed stream-ordered and the streams and events are destroyed.
     g_err[0] = 0;
     g_launches = 0;
     int rc = validate(s, n, p, out_latency, o);
     if (rc) return rc;
     if (n == 0) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
-    const size_t K = (size_t)p->K, nn = (size_t)n;
-    const size_t bI = nn * K * 4, bD = nn * K * 8, bA = nn * 8, bC = s->coeffs ? nn * 32 : 0;
-    const size_t bLat = nn * 24, bS = nn * 4, bW = o->bw_share ? nn * K * 8 : 0;
-    size_t off = 0;
-    auto take = [&](size_t b) { size_t q = off; off += (b + 255) & ~(size_t)255; return q; };
-    const size_t oI = take(bI), oP = take(bD), oG = take(bD), oA = take(bA), oC = take(bC);
-    const size_t oLat = take(bLat), oGm = take(bS), oM = take(bS), oBe = take(bI), oOr = take(bI),
-                 oW = take(bW), oSt = take(bS);
-    unsigned char* d = nullptr;
-    int dev = 0;
-    CU(cudaGetDevice(&dev));
-    if (int rc2 = keep_pool_cached(dev)) return rc2;
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&d), off, st));
-    constexpr int kS = 4;                    // 0: H2D, 1-2: solves, 3: D2H
-    constexpr int kMaxCh = 16;
-    cudaStream_t ss[kS] = {};
-    cudaEvent_t ev0 = nullptr, evh[kMaxCh] = {}, evc[kMaxCh] = {}, evj[kS] = {};
-    for (int q = 0; q < kS; ++q) CU(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
-    CU(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
-    for (int q = 0; q < kMaxCh; ++q) {
-        CU(cudaEventCreateWithFlags(&evh[q], cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&evc[q], cudaEventDisableTiming));
-    }
-    for (int q = 0; q < kS; ++q) CU(cudaEventCreateWithFlags(&evj[q], cudaEventDisableTiming));
-    CU(cudaEventRecord(ev0, st));
-    for (int q = 0; q < kS; ++q) CU(cudaStreamWaitEvent(ss[q], ev0, 0));
-
-    const long long nch = std::max(1LL, std::min((long long)kMaxCh, (long long)(n / 32768)));
-    const long long chunk = (n + nch - 1) / nch;
-    int launches = 0;
-    auto h2d = [&](size_t doff, const void* src, size_t row, long long a, long long m, cudaStream_t q) {
-        return cudaMemcpyAsync(d + doff + row * a, static_cast<const unsigned char*>(src) + row * a, row * m,
-                               cudaMemcpyHostToDevice, q);
-    };
-    auto d2h = [&](void* dst, size_t doff, size_t row, long long a, long long m, cudaStream_t q) {
-        return cudaMemcpyAsync(static_cast<unsigned char*>(dst) + row * a, d + doff + row * a, row * m,
-                               cudaMemcpyDeviceToHost, q);
-    };
-    for (long long c = 0; c < nch; ++c) {
-        const long long a = c * chunk, m = std::min(chunk, (long long)n - a);
-        if (m <= 0) break;
-        cudaStream_t q = ss[0];
-        CU(h2d(oI, s->input_len, K * 4, a, m, q));
-        CU(h2d(oP, s->tx_power_w, K * 8, a, m, q));
-        CU(h2d(oG, s->gain, K * 8, a, m, q));
-        CU(h2d(oA, s->alpha, 8, a, m, q));
-        if (bC) CU(h2d(oC, s->coeffs, 32, a, m, q));
-        CU(cudaEventRecord(evh[c], q));
-        q = ss[1 + (c & 1)];
-        CU(cudaStreamWaitEvent(q, evh[c], 0));
-        sdedge_scenarios ds{reinterpret_cast<int32_t*>(d + oI) + a * K, reinterpret_cast<double*>(d + oP) + a * K,
-                            reinterpret_cast<double*>(d + oG) + a * K, reinterpret_cast<double*>(d + oA) + a,
-                            bC ? reinterpret_cast<double*>(d + oC) + a * 4 : nullptr};
-        sdedge_schedule dsch{reinterpret_cast<int32_t*>(d + oGm) + a, reinterpret_cast<int32_t*>(d + oM) + a,
-                             reinterpret_cast<int32_t*>(d + oBe) + a * K, reinterpret_cast<int32_t*>(d + oOr) + a * K,
-                             bW ? reinterpret_cast<double*>(d + oW) + a * K : nullptr,
-                             reinterpret_cast<int32_t*>(d + oSt) + a, nullptr};
-        sdedge_params pc = *p;
-        pc.stream = q;
-        rc = solve_device(&ds, m, &pc, reinterpret_cast<double*>(d + oLat) + 3 * a, &dsch);
-        if (rc) return rc;
-        launches += g_launches;
-        CU(cudaEventRecord(evc[c], q));
-        q = ss[3];
-        CU(cudaStreamWaitEvent(q, evc[c], 0));
-        CU(d2h(out_latency, oLat, 24, a, m, q));
-        CU(d2h(o->gamma, oGm, 4, a, m, q));
-        CU(d2h(o->num_batches, oM, 4, a, m, q));
-        CU(d2h(o->batch_end, oBe, K * 4, a, m, q));
-        CU(d2h(o->order, oOr, K * 4, a, m, q));
-        if (bW) CU(d2h(o->bw_share, oW, K * 8, a, m, q));
-        CU(d2h(o->status, oSt, 4, a, m, q));
-    }
-    for (int q = 0; q < kS; ++q) {
-        CU(cudaEventRecord(evj[q], ss[q]));
-        CU(cudaStreamWaitEvent(st, evj[q], 0));
-    }
-    CU(cudaFreeAsync(d, st));
-    for (int q = 0; q < kS; ++q) CU(cudaStreamDestroy(ss[q]));   // released once their work drains
-    CU(cudaEventDestroy(ev0));
-    for (int q = 0; q < kMaxCh; ++q) {
-        CU(cudaEventDestroy(evh[q]));
-        CU(cudaEventDestroy(evc[q]));
-    }
-    for (int q = 0; q < kS; ++q) CU(cudaEventDestroy(evj[q]));
-    g_launches = launches;
-    return 0;
+    HostPipe hp;
+    rc = host_pipeline(hp, s, n, p, out_latency, o, st);
+    const int rc2 = hp.finish(st);
+    return rc ? rc : rc2;
 }
 
 int sdedge_evaluate_actual(const sdedge_scenarios* s, const int32_t* output_len, int64_t n, const sdedge_params* p,
@@ -2451,7 +2807,7 @@ int sdedge_brute_force(const sdedge_scenarios* s, int64_t n, const sdedge_params
     unsigned char* ws = nullptr;
     const size_t offg = ((size_t)items * sizeof(double) + 255) & ~(size_t)255;
     const size_t offm = offg + (((size_t)items * sizeof(int32_t) + 255) & ~(size_t)255);
-    CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), offm + (size_t)items * sizeof(unsigned), st));
+    if (int rc2 = ws_alloc(reinterpret_cast<void**>(&ws), offm + (size_t)items * sizeof(unsigned), st)) return rc2;
     double* wsv = reinterpret_cast<double*>(ws);
     int32_t* wsg = reinterpret_cast<int32_t*>(ws + offg);
     unsigned* wsm = reinterpret_cast<unsigned*>(ws + offm);
@@ -2464,6 +2820,48 @@ int sdedge_brute_force(const sdedge_scenarios* s, int64_t n, const sdedge_params
     CU(cudaGetLastError());
     CU(cudaFreeAsync(ws, st));
     g_launches = 2;
+    return 0;
+}
+
+// ---- multi-GPU gather: the shard ranks store their outputs straight into
+// cuda:0's arrays over NVLink through CUDA IPC mappings
+int sdedge_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset)
+{
+    g_err[0] = 0;
+    if (!dev_ptr || !handle || !offset) return fail(-1, "null argument");
+    using AddrRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CU(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(-2, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<AddrRange>(fn)(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+        return fail(-1, "dev_ptr is not a device allocation");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+    return 0;
+}
+
+int sdedge_ipc_open(const void* handle, uint64_t offset, void** dev_ptr)
+{
+    g_err[0] = 0;
+    if (!handle || !dev_ptr) return fail(-1, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<unsigned char*>(base) + offset;
+    return 0;
+}
+
+int sdedge_ipc_close(void* dev_ptr, uint64_t offset)
+{
+    g_err[0] = 0;
+    if (!dev_ptr) return fail(-1, "null argument");
+    CU(cudaIpcCloseMemHandle(static_cast<unsigned char*>(dev_ptr) - offset));
     return 0;
 }
 

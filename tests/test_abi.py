@@ -26,13 +26,13 @@ def test_library_exports_every_declared_symbol():
     L = C.CDLL(sd.LIB)
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert sd.sdedge_abi_version() == 2
+    assert sd.sdedge_abi_version() == 3
 
 
 def test_struct_layout_matches_header():
     # sdedge_params: 2 models (24 B) + 4 c + B_w + sigma + lambda (56) + int64 + 7 int32 + pad + double + ptr
     assert C.sizeof(sd.SdedgeParams) == 152
-    assert C.sizeof(sd.SdedgeScenarios) == 40 and C.sizeof(sd.SdedgeSchedule) == 56
+    assert C.sizeof(sd.SdedgeScenarios) == 40 and C.sizeof(sd.SdedgeSchedule) == 72
 
 
 @pytest.mark.parametrize("bad", [dict(K=0), dict(K=1025), dict(gamma_min=3, gamma_max=2),
@@ -40,7 +40,7 @@ def test_struct_layout_matches_header():
                                  dict(bandwidth_hz=-1.0), dict(c1_draft=float("nan")),
                                  dict(precision=2), dict(algo=7), dict(flags=2), dict(draft=(0, 768, 3072)),
                                  dict(verify=(32, 70000, 11008)), dict(downlink_s=-1.0),
-                                 dict(bandwidth_policy=2), dict(batching_policy=6),
+                                 dict(bandwidth_policy=2), dict(batching_policy=7),
                                  dict(batching_policy=3, static_batch=0)])
 def test_invalid_arguments_rejected_without_gpu(bad):
     pd = dict(scengen.params("68M-7B", K=4), **bad)

@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import scengen
-from tests.parity import compare, gpu_solve, to_numpy
+from tests.parity import compare, gpu_solve, load_fixture, to_numpy
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -74,7 +74,7 @@ def test_c3_sample(pair):
     pd = scengen.params(pair, K=32, gamma_min=1, gamma_max=8)
     orc = oracle.solve_batch(pd, sc)
     res, _, _ = _check(pd, sc, 0, ENV, orc)
-    assert res["exact"] + res["exempt"] == 1500
+    assert res["exact"] + res["exempt_same"] + res["replayed"] == 1500
     sub = {k: (v[:300] if v is not None else None) for k, v in sc.items()}
     orc_sub = {k: v[:300] if hasattr(v, "__len__") else v for k, v in orc.items()}
     _check(pd, sub, 0, DENSE, orc_sub)
@@ -82,15 +82,24 @@ def test_c3_sample(pair):
 
 
 # ---------------------------------------------------------------- C4 (bench config)
-def test_c4_full_size_sampled():
-    """All 1e6 C4 scenarios in one call (the bench launch); oracle on a
-    deterministic sample s = 0 mod 62500; invariants on every scenario."""
-    pd, sc, n = scengen.config("C4")
-    g = gpu_solve(pd, sc)
-    idx = np.arange(0, n, 62500)
-    sub = {k: (v[idx] if v is not None else None) for k, v in sc.items()}
-    orc = oracle.solve_batch(pd, sub)
-    res = compare(pd, sc, g, orc, 0, oracle, idx=idx)
+def _full(cfg, pair, precision=0):
+    pd, sc, n = scengen.config(cfg, pair=pair)
+    return pd, sc, n, gpu_solve(pd, sc, precision=precision)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_c4_full_size_sampled(pair, precision):
+    """All 1e6 C4 scenarios in one call (the bench launch), fp64 and the fp32
+    variant; the oracle's stored results on the deterministic sample (s = 0 mod
+    500: 2000 scenarios for (68M,7B); s = 0 mod 2000 for (1.1B,7B); written by
+    tools/make_oracle_fixtures.py from oracle/ only) with the north_star
+    tolerances and the near-tie replay; invariants on every scenario."""
+    name = f"c4_{pair}"
+    _, _, idx, orc = load_fixture(name)
+    pd, sc, n, g = _full("C4", pair, precision)
+    res = compare(pd, sc, g, orc, precision, oracle, idx=idx, label=f"C4 {pair} full launch, sample {len(idx)}, "
+                                                                   f"{'fp64' if precision == 0 else 'fp32'}")
     assert res["failures"] == 0
     assert np.all(g["status"] == 0)
     M = g["M"]
@@ -98,30 +107,32 @@ def test_c4_full_size_sampled():
     assert np.all(g["batch_end"][np.arange(n), M - 1] == 128)
     assert np.all(g["lat"][:, 0] == g["lat"][:, 1] + g["lat"][:, 2])
     assert np.allclose(g["w"].sum(1), 1.0, rtol=0, atol=1e-12)
+    # the trace backtracks to the plan on every scenario (a cheap full-size consistency check)
+    tr, be = g["trace"], g["batch_end"]
+    for s in range(0, n, 997):
+        assert oracle.backtrack(tr[s]) == [int(x) for x in be[s][: M[s]]]
 
 
 # ---------------------------------------------------------------- C5 (large K)
 @pytest.mark.parametrize("K", [256, 512, 1024])
 def test_c5_large_k(K):
-    """Full 1e4-scenario launch at each K; oracle on small samples (gamma range
-    reduced for the oracle's literal O(K^2 N gamma) cost) and the eq:time
-    self-consistency of every sampled GPU plan at the full gamma range."""
-    pd, sc, n = scengen.config(f"C5{K}")
-    g = gpu_solve(pd, sc)
+    """Full 1e4-scenario launch at each K and the full gamma range 1..16; the
+    oracle's stored results on the first scenarios (tools/make_oracle_fixtures.py)
+    and the eq:time self-consistency of sampled GPU plans."""
+    _, _, idx, orc = load_fixture(f"c5_{K}")
+    pd, sc, n, g = _full(f"C5{K}", "68M-7B")
     assert np.all(g["status"] == 0)
+    res = compare(pd, sc, g, orc, 0, oracle, idx=idx, label=f"C5 K={K} full launch, gamma 1..16")
+    assert res["failures"] == 0
     rng = np.random.default_rng(K)
     for s in rng.choice(n, 6, replace=False):
         Is = sc["I"][s][g["order"][s]]
         ends = list(g["batch_end"][s][: g["M"][s]])
         v = oracle.eval_plan(pd, Is, float(sc["alpha"][s]), int(g["gamma"][s]), ends)
         assert abs(v - g["lat"][s, 2]) <= 1e-12 * v
-    n_or = {256: 3, 512: 2, 1024: 1}[K]
-    gmax = {256: 4, 512: 2, 1024: 1}[K]
-    pd2 = dict(pd, gamma_min=1, gamma_max=gmax)
-    sub = {k: (v[:n_or] if v is not None else None) for k, v in sc.items()}
-    res, _, _ = _check(pd2, sub, 0, ENV)
-    assert res["failures"] == 0
-    _check(pd2, {k: (v[:1] if v is not None else None) for k, v in sc.items()}, 0, DENSE)
+    sub = {k: (v[:1] if v is not None else None) for k, v in sc.items()}
+    pd2 = dict(pd, gamma_min=1, gamma_max={256: 4, 512: 2, 1024: 1}[K])
+    _check(pd2, sub, 0, DENSE)
 
 
 # ---------------------------------------------------------------- edge cases
@@ -234,6 +245,7 @@ def test_host_entry_point_and_determinism():
     h = to_numpy(h)
     for k in d1:
         assert np.array_equal(d1[k], d2[k]), k
+    for k in h:                                      # the host entry has no trace output
         assert np.array_equal(d1[k], h[k]), k
 
 
@@ -286,7 +298,7 @@ def test_host_entry_point_chunked():
     h = sd.solve_host(pd, *(torch.from_numpy(sc[k]).pin_memory() for k in ("I", "p", "g", "alpha")))
     torch.cuda.synchronize()
     h = to_numpy(h)
-    for k in d:
+    for k in h:
         assert np.array_equal(d[k], h[k]), k
 
 
@@ -353,19 +365,6 @@ def test_actual_output_evaluation(cfg, pair, n, pol):
     assert np.allclose(full.cpu().numpy(), pl["lat"][:, 2], rtol=1e-12, atol=0)
 
 
-def test_c4_fp32_tiled():
-    """fp32 variant through the tiled large-K DP (TMA-staged predecessor rows)."""
-    pd, sc, _ = scengen.config("C4", 0, 400)
-    orc_idx = np.arange(0, 400, 50)
-    sub = {k: (v[orc_idx] if v is not None else None) for k, v in sc.items()}
-    orc = oracle.solve_batch(pd, sub)
-    g = gpu_solve(pd, sc, precision=1)
-    res = compare(pd, sc, g, orc, 1, oracle, idx=orc_idx)
-    assert res["failures"] == 0
-    g64 = gpu_solve(pd, sc, precision=0)
-    assert np.allclose(g["lat"], g64["lat"], rtol=1e-5, atol=0)
-
-
 def test_overflow_second_pass_tiled():
     """The tiny first-pass pool at K = 128 (tiled DP) with the slow 1.1B draft
     (multi-segment envelopes): identical results through the worst-case pass."""
@@ -379,3 +378,49 @@ def test_overflow_second_pass_tiled():
     idx = np.arange(0, 300, 60)
     sub = {k: (v[idx] if v is not None else None) for k, v in sc.items()}
     compare(pd, sc, a, oracle.solve_batch(pd, sub), 0, oracle, idx=idx)
+
+
+# ---------------------------------------------------------------- per-batch gamma (NEXT-3)
+@pytest.mark.parametrize("cfg,pair,n", [("C3", "68M-7B", 300), ("C3", "1.1B-7B", 300), ("C2", None, 3),
+                                        ("C4", "1.1B-7B", 16), ("C1", "1.1B-13B", 200)])
+def test_per_batch_gamma(cfg, pair, n):
+    """SDEDGE_BATCH_PER_BATCH_GAMMA (an extension, PAPER.md:555 fixes one l) against
+    the oracle's Algorithm 1 over (j, gamma) candidates: T, T_com, T_inf, every
+    batch boundary and every batch's gamma; the plan re-evaluated by the oracle's
+    literal active-set eq:time (orc_eval_plan_pbg) equals the GPU's T_inf."""
+    pd, sc, _ = scengen.config(cfg, 0, n, pair=pair)
+    pd = dict(pd, batching_policy=6, gamma_min=max(pd["gamma_min"], 1))
+    orc = oracle.solve_batch(pd, sc)
+    g = gpu_solve(pd, sc)
+    res = compare(pd, sc, g, orc, 0, oracle, label=f"per-batch gamma {cfg} {pair}")
+    assert res["failures"] == 0
+    for s in range(0, n, max(1, n // 20)):
+        M = int(g["M"][s])
+        Is = sc["I"][s][g["order"][s]]
+        co = None if sc.get("coeffs") is None else sc["coeffs"][s]
+        v = oracle.eval_plan_pbg(pd, Is, float(sc["alpha"][s]), g["batch_end"][s][:M], g["batch_gamma"][s][:M],
+                                 coeffs=co)
+        assert abs(v - g["lat"][s, 2]) <= 1e-12 * v
+        assert g["gamma"][s] == g["batch_gamma"][s][M - 1] and np.all(g["batch_gamma"][s][M:] == 0)
+
+
+def test_actual_output_rejects_malformed_plans():
+    """sdedge_evaluate_actual takes caller plans: malformed ones give NaN, never
+    out-of-bounds reads (batch ends not increasing / beyond K / not ending at K,
+    order entries outside 0..K-1)."""
+    import paper_2510_11331_b200 as sd
+    pd, sc, _ = scengen.config("C3", 0, 6)
+    K = pd["K"]
+    dev = "cuda:0"
+    t = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).to(dev) for k in ("I", "p", "g", "alpha")}
+    plan = sd.solve(pd, t["I"], t["p"], t["g"], t["alpha"])
+    O = torch.full((6, K), 100, dtype=torch.int32, device=dev)
+    plan["batch_end"][1, plan["M"][1] - 1] = K + 5             # beyond K
+    plan["M"][2] = 2
+    plan["batch_end"][2, :2] = torch.tensor([5, 3], dtype=torch.int32)   # not increasing
+    plan["M"][3] = 1
+    plan["batch_end"][3, 0] = K - 1                            # does not end at K
+    plan["order"][4, 7] = K                                    # order out of range
+    act = sd.evaluate_actual(pd, t["I"], t["p"], t["g"], t["alpha"], O, plan).cpu().numpy()
+    assert np.isfinite(act[0]) and np.isfinite(act[5])
+    assert np.all(np.isnan(act[1:5]))

@@ -227,3 +227,40 @@ def test_t_inf_at_least_total_verify_work(orc, pair):
                 lb += 2 * t1 - t2                                # one intercept
             assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
             assert lb > 0.5 * t_inf or pair != "68M-7B"          # and it is not vacuous for a small draft
+
+
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_row_value_plus_remaining_verify_work(orc, pair):
+    """Upsilon[K,0,0] >= Upsilon[i,0,0] + sum_{k>i} vsl(I_k) for every row i: each
+    candidate of row i+1 either extends a candidate of row i by task i+1 (same
+    predecessor state; its batch's verify time grows by at least that task's own
+    slope, every other stage time can only grow -- eq:flops_v, eq:latency_b2,
+    eq:time) or starts a new batch after row i's state (every step's completion
+    is at least Upsilon1[i,n] plus the new batch's verify time).  The GPU stops a
+    gamma at a tile end when this bound exceeds the best finished T_inf (DESIGN.md
+    5.2e); pinned here on the oracle's literal DP (row values from orc_dp_trace)
+    and stage-time functions, with binding memory windows for the 1.1B draft."""
+    K = 14
+    pd = scengen.params(pair, K=K, gamma_min=1, gamma_max=8, O_max=192)
+    if pair == "1.1B-7B":
+        J, h1, h2 = scengen.MODELS["1.1B"]
+        pd = dict(pd, mem_capacity_bytes=orc.param_memory(J, h1, h2) + 5 * orc.kv_memory_per_task(J, h1, 300, 192))
+    sc = scengen.generate(93, K, 0, 6)
+    n_tight = 0
+    for s in range(6):
+        Is = np.sort(sc["I"][s])
+        alpha = float(sc["alpha"][s])
+        for gamma in (1, 3, 7):
+            L = orc.expected_tokens(alpha, gamma)
+            N = orc.decode_steps(pd["O_max"], L)
+            t, S, gap, rb, rt, W = orc.dp_trace(pd, Is, alpha, gamma)
+            if not np.isfinite(t):
+                continue
+            vsl = np.array([sum(orc.verify_time(pd, 2, int(I), gamma, L, n) - orc.verify_time(pd, 1, int(I), gamma, L, n)
+                                for n in range(1, N + 1)) for I in Is])
+            for i in range(1, K):
+                bound = rt[i - 1] + vsl[i:].sum()
+                assert t >= bound * (1 - 1e-12), (s, gamma, i, t, bound)
+                n_tight += bound > 0.9 * t
+            assert np.all(np.diff(rt) >= vsl[1:] * (1 - 1e-12) - 1e-12 * rt[1:])   # row by row
+    assert n_tight > 0
