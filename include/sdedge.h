@@ -70,6 +70,11 @@ typedef enum {
 } sdedge_algo;
 
 #define SDEDGE_FLAG_TINY_POOL 1
+/* SDEDGE_BATCH_HEURISTIC reading: equal batches of size b with b growing while the latency
+ * improves; by default from b = 2 (reading B5), with this flag from two batches,
+ * b = ceil(K/2) (reading B5') -- "begins with two batches, progressively
+ * increases the batch size". */
+#define SDEDGE_FLAG_HEURISTIC_HALF 2
 
 /* Bandwidth policies (P:580-616 and the uniform baseline of P:936-940). */
 typedef enum {
@@ -110,8 +115,9 @@ typedef struct {
                                     gamma = 0 is the autoregressive reduction)               */
     int32_t precision;           /* 0 = fp64 DP arithmetic, 1 = fp32 variant                 */
     int32_t algo;                /* sdedge_algo                                              */
-    int32_t flags;               /* 0, or SDEDGE_FLAG_TINY_POOL (test hook: an 8-segment first-pass
-                                    envelope pool, forcing the worst-case second pass)       */
+    int32_t flags;               /* bit set: SDEDGE_FLAG_TINY_POOL (test hook: an 8-segment first-pass
+                                    envelope pool, forcing the worst-case second pass),
+                                    SDEDGE_FLAG_HEURISTIC_HALF (heuristic batching reading)  */
     double  downlink_s;          /* >= 0, added to every verify stage (P:424-427 says 0)     */
     void*   stream;              /* cudaStream_t                                              */
     int32_t bandwidth_policy;    /* sdedge_bw_policy (0 = the paper's policy)                 */

@@ -34,7 +34,8 @@ class Params(C.Structure):
                 ("Bw", C.c_double), ("sigma2", C.c_double), ("lambda_", C.c_double),
                 ("gamma_s", C.c_int64), ("K", C.c_int32), ("O_max", C.c_int32),
                 ("gamma_min", C.c_int32), ("gamma_max", C.c_int32), ("downlink_s", C.c_double),
-                ("bw_policy", C.c_int32), ("batch_policy", C.c_int32), ("static_batch", C.c_int32)]
+                ("bw_policy", C.c_int32), ("batch_policy", C.c_int32), ("static_batch", C.c_int32),
+                ("heuristic_start", C.c_int32)]
 
 
 class Result(C.Structure):
@@ -115,7 +116,7 @@ def make_params(d: dict) -> Params:
                   d["c2_verify"], d["bandwidth_hz"], d["noise_w"], d.get("lambda_bits", 0.0),
                   int(d["mem_capacity_bytes"]), d["K"], d["O_max"], d["gamma_min"], d["gamma_max"],
                   d.get("downlink_s", 0.0), d.get("bandwidth_policy", 0), d.get("batching_policy", 0),
-                  d.get("static_batch", 4))
+                  d.get("static_batch", 4), d.get("heuristic_start", 0))
 
 
 def _p(a, t):

@@ -293,12 +293,15 @@ int orc_fixed_plan(const orc_params* P, const double* co, const int32_t* Is, dou
         M = equal_plan(K, b, ends);
         break;
     }
-    case 5: { /* heuristic (reading B5): batch size 2, 3, ... until the
-                 pipelined latency stops improving (or memory binds) */
+    case 5: { /* heuristic: equal batches of size b, b growing until the
+                 pipelined latency stops improving (or memory binds); reading B5 starts at
+                 b = 2, reading B5' (heuristic_start = 1) at two batches,
+                 b = ceil(K/2) */
         int32_t tmp[1024 + 1];
         int bbest = 1;
         double tbest = INFINITY;
-        for (int b = (K >= 2 ? 2 : 1); b <= K; ++b) {
+        const int b0 = P->heuristic_start ? (K + 1) / 2 : (K >= 2 ? 2 : 1);
+        for (int b = b0; b <= K; ++b) {
             int Mt = equal_plan(K, b, tmp);
             double t = orc_eval_plan(P, co, Is, alpha, gamma, Mt, tmp);
             if (!(t < tbest) && !isinf(tbest)) break;   /* latency starts to degrade */

@@ -38,6 +38,8 @@ typedef struct {
                                     4 max batching, 5 heuristic,
                                     6 per-batch gamma (an extension) */
     int32_t static_batch;        /* batch size of policy 3                          */
+    int32_t heuristic_start;     /* policy 5: 0 sizes 2, 3, ... (reading B5); 1 from two batches,
+                                    ceil(K/2), upward (reading B5')      */
 } orc_params;
 
 typedef struct {

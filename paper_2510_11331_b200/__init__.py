@@ -19,7 +19,7 @@ __all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_act
 ALGO_ENVELOPE, ALGO_DENSE = 0, 1
 BW_OPTIMAL, BW_UNIFORM = 0, 1
 BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC, BATCH_PER_BATCH_GAMMA = range(7)
-FLAG_TINY_POOL = 1
+FLAG_TINY_POOL, FLAG_HEURISTIC_HALF = 1, 2
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
                     "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
                     "sdedge_abi_version", "sdedge_pipe_peak", "sdedge_ipc_export", "sdedge_ipc_open",
@@ -112,7 +112,8 @@ def make_params(d: dict, stream=None, precision: int | None = None, algo: int | 
                         d["bandwidth_hz"], d["noise_w"], d.get("lambda_bits", 0.0),
                         int(d["mem_capacity_bytes"]), d["K"], d["O_max"], d["gamma_min"], d["gamma_max"],
                         d.get("precision", 0) if precision is None else precision,
-                        d.get("algo", ALGO_ENVELOPE) if algo is None else algo, d.get("flags", 0),
+                        d.get("algo", ALGO_ENVELOPE) if algo is None else algo,
+                        d.get("flags", 0) | (FLAG_HEURISTIC_HALF if d.get("heuristic_start", 0) else 0),
                         d.get("downlink_s", 0.0), st, d.get("bandwidth_policy", 0),
                         d.get("batching_policy", 0), d.get("static_batch", 4), 0)
 

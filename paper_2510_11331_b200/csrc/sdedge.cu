@@ -47,10 +47,13 @@ int fail(int code, const char* msg)
 #endif
 constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_G
-#define SDEDGE_TILE_G 2       // DPs per warp of the tiled DP (tile = 32 / G rows)
+#define SDEDGE_TILE_G 1       // DPs per warp of the tiled DP (tile = 32 / G rows)
 #endif
 #ifndef SDEDGE_TILE_SHFL_ARGMIN
 #define SDEDGE_TILE_SHFL_ARGMIN 1
+#endif
+#ifndef SDEDGE_RS_MAX_K
+#define SDEDGE_RS_MAX_K 160   // tiled DP keeps its row store in shared memory up to this K
 #endif
 #ifndef SDEDGE_TILE_MIN_K
 #define SDEDGE_TILE_MIN_K 0   // tiled DP above this K (all K since the push-style phase B)
@@ -69,6 +72,7 @@ struct Consts {
     double Bw, sigma2, lambda, dl;
     long long gamma_s, Gp, kvunit;       // Gamma_s, Gamma_p (eq:memory_model), 4 Jd hd
     int bw_policy, batch_policy, static_batch;   // SDEDGE_BW_* / SDEDGE_BATCH_* (paper baselines)
+    int flags;                           // SDEDGE_FLAG_*
     int rows_in_smem;                    // DP row state in shared (1) or global (0) memory
     long long pool_cap;                  // envelope segments per warp slot
     long long rows_stride;               // bytes of one warp's global row state
@@ -101,22 +105,20 @@ struct Outputs {
 // each DP (warp-reduced), not carried in registers across the gamma loop.
 // Slots: candidates, candidate-segments, candidate-steps W, rows, full evaluations.
 struct WorkCount {
-    unsigned long long* sh;
+    unsigned long long* sh;        // this thread's 5 slots in shared memory, or null (not counted)
 };
 
+// Each thread adds its own counts to its own shared slots -- no atomics, no shuffles on the
+// hot path; the CTA reduces its slots once, at exit, when the caller asked for counters.
 __device__ inline void work_flush(const WorkCount& wc, bool active, unsigned cand, unsigned seg, unsigned full,
                                   unsigned long long steps, unsigned rows)
 {
-    unsigned long long v[5] = {active ? cand : 0u, active ? seg : 0u, active ? steps : 0ull, active ? rows : 0u,
-                               active ? full : 0u};
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
-    }
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int q = 0; q < 5; ++q) atomicAdd(wc.sh + q, v[q]);
+    if (!wc.sh || !active) return;
+    wc.sh[0] += cand;
+    wc.sh[1] += seg;
+    wc.sh[2] += steps;
+    wc.sh[3] += rows;
+    wc.sh[4] += full;
 }
 
 struct Work {
@@ -432,6 +434,76 @@ __device__ inline DPConst make_dpconst(const Consts& C, int gamma, double L, int
     return D;
 }
 
+// First feasible batch start j of row i (cons. (b), Alg. 1 lines 10-13): batches of
+// b <= bmax = floor(room / d) tasks fit, room = Gamma_s - Gamma_p, d = 4 Jd hd (I + O_max).
+// Exact integer floor; below 2^52 it is a double division (correctly rounded, so at most one
+// too high) with an exact integer fix-up instead of a 64-bit integer division.
+__device__ inline int window_lo(long long room, long long d, int i)
+{
+    long long bmax = 0;
+    if (room >= 0 && d > 0) {
+        if (room < (1LL << 52) && d < (1LL << 52)) {
+            bmax = (long long)((double)room / (double)d);
+            if (bmax * d > room) --bmax;
+        } else {
+            bmax = room / d;
+        }
+    }
+    return bmax >= i ? 1 : (int)(i - bmax + 1);
+}
+
+// Warp-register bitonic sort of 32 E 64-bit keys (element e = lane E + r in register r):
+// partners at distance st >= E are in lane ^ (st / E) (shuffles), smaller distances in the
+// same lane -- no shared-memory traffic and no barriers.
+template <int E>
+__device__ inline void warp_bitonic(unsigned long long (&x)[E], int lane)
+{
+    constexpr int P = 32 * E;
+#pragma unroll
+    for (int sz = 2; sz <= P; sz <<= 1) {
+#pragma unroll
+        for (int st = sz >> 1; st > 0; st >>= 1) {
+            if (st >= E) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int e = lane * E + r;
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, x[r], st / E);
+                    const bool keep_min = ((e & sz) == 0) == ((e & st) == 0);   // ascending half's lower element
+                    x[r] = keep_min ? (o < x[r] ? o : x[r]) : (o > x[r] ? o : x[r]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    if (r & st) continue;
+                    const unsigned long long a = x[r], b = x[r | st];
+                    if ((a > b) == (((lane * E + r) & sz) == 0)) { x[r] = b; x[r | st] = a; }
+                }
+            }
+        }
+    }
+}
+
+template <int E>
+__device__ inline void warp_sort_tasks(const int* I, int* ord, int* Is, int K, int lane)
+{
+    unsigned long long x[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int e = lane * E + r;
+        x[r] = e < K ? ((unsigned long long)((unsigned)I[e] ^ 0x80000000u) << 32) | (unsigned)e : ~0ULL;
+    }
+    warp_bitonic<E>(x, lane);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int e = lane * E + r;
+        if (e < K) {
+            const int k = (int)(unsigned)(x[r] & 0xffffffffULL);
+            ord[e] = k;
+            Is[e] = I[k];
+        }
+    }
+}
+
 // ------------------------------------------------------------ shared layout
 struct Smem {
     int* I;        // [K] original lengths
@@ -440,8 +512,8 @@ struct Smem {
     unsigned long long* key;  // [sort_len(K)] bitonic sort keys (biased I_k << 32 | k)
     double* glb;   // [ng] pre-DP lower bound of T_inf(gamma), in gamma-index order
     int* gord;     // [ng] gamma indices in the order the warps take them (most promising first)
-    double* pI;    // [K+1] prefix sums of the sorted I (exact integers), pI[0] = 0
-    double* pI2;   // [K+1] prefix sums of the sorted I^2
+    double* pI;    // [K/kPfx + 2] prefix sums of the sorted I (exact integers) at rows 0, kPfx, 2 kPfx, ..
+    double* pI2;   // [K/kPfx + 2] ... of the sorted I^2 (the last entry: the total)
     int* nq;       // [ng] N_gamma (per-batch-gamma policy)
     DPConst* dq;   // [ng] stage-time constants per gamma (per-batch-gamma policy)
     short* jlo;    // [K] first feasible j of row i (memory window), > i if none
@@ -467,6 +539,16 @@ __host__ __device__ inline size_t tile_bytes()
            2 * (size_t)kTileCh * sizeof(RowRec<R>) + 2 * sizeof(unsigned long long) + sizeof(DPConst);
 }
 
+// rows past K that the shared-memory row store needs so that every tile of GL rows is in bounds
+__host__ __device__ inline int rs_pad(int K, int GL)
+{
+    return (K + GL - 1) / GL * GL - K;
+}
+
+// prefix sums of I and I^2 are kept at rows 0, 16, 32, ... (the tile ends, GL in {8, 16, 32})
+constexpr int kPfx = 8;
+__host__ __device__ inline int pfx_len(int K) { return K / kPfx + 2; }
+
 // bitonic sort length: the next power of two >= K
 __host__ __device__ inline int sort_len(int K)
 {
@@ -476,7 +558,7 @@ __host__ __device__ inline int sort_len(int K)
 }
 
 template <typename R, int G>
-__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile)
+__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile, int row_pad = 0)
 {
     size_t b = 0;
     b += 3 * (size_t)K * sizeof(int);
@@ -485,12 +567,12 @@ __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, in
     b += (size_t)ng * (sizeof(double) + 2 * sizeof(int));
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(DPConst);
-    b += 2 * (size_t)(K + 1) * sizeof(double);
+    b += 2 * (size_t)pfx_len(K) * sizeof(double);
     b += (size_t)(2 + kWarps) * K * sizeof(short);
     b = (b + 15) & ~(size_t)15;
     b += (size_t)ng * sizeof(double) + 5 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
     b = (b + 15) & ~(size_t)15;
-    if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K);
+    if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K + row_pad);
     if (tile) b += (size_t)kWarps * G * tile_bytes<R, G>();
     return b;
 }
@@ -509,8 +591,8 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     s.nq = reinterpret_cast<int*>(base + b); b += (size_t)ng * sizeof(int);
     b = (b + 15) & ~(size_t)15;
     s.dq = reinterpret_cast<DPConst*>(base + b); b += (size_t)ng * sizeof(DPConst);
-    s.pI = reinterpret_cast<double*>(base + b); b += (size_t)(K + 1) * sizeof(double);
-    s.pI2 = reinterpret_cast<double*>(base + b); b += (size_t)(K + 1) * sizeof(double);
+    s.pI = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * sizeof(double);
+    s.pI2 = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * sizeof(double);
     s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jf = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
     s.jw = reinterpret_cast<short*>(base + b); b += (size_t)kWarps * K * sizeof(short);
@@ -1203,7 +1285,7 @@ __device__ int row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g
         const R2<R> E{rest, cntp == 0 ? (R)0 : (R)Mx};
         const R key = d1 + rest;
         o_s->Y = Y; o_s->A = A; o_s->E = E; o_s->Ln = Ln; o_s->cnt = cntp; o_s->off = 0; o_s->key = key;
-        o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0; o_g->key = key;
+        if (o_g != o_s) { o_g->Y = Y; o_g->A = A; o_g->E = E; o_g->Ln = Ln; o_g->cnt = cntp; o_g->off = 0; o_g->key = key; }
         return 0;
     }
     if (spec) return 2;
@@ -1214,7 +1296,7 @@ __device__ int row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g
     const bool ovf = row_merge_rec(q, o_s, pl, P, Q, Av, Bv, rest, Mx, top);
     o_s->key = d1 + rest;
     *top_s = top;
-    *o_g = *o_s;
+    if (o_g != o_s) *o_g = *o_s;
     return ovf ? 1 : 0;
 }
 
@@ -1227,12 +1309,13 @@ __device__ int row_update_rec(const RowRec<R>* q, RowRec<R>* o_s, RowRec<R>* o_g
 // as predecessor.  Every lane sees its row's candidates in ascending j, so the
 // '<=' update keeps the largest j: the same candidates, comparisons and tie
 // rule as dp_gamma.
-template <typename R, int G>
-__device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, RowRec<R>* tb,
+// RS: the row store itself lives in shared memory (small K): phase A reads the finished rows in
+// place and the tile's rows are rows i0.. of the store -- no TMA staging, no global row traffic.
+template <typename R, int G, bool RS>
+__device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<R> pl, RowRec<R>* tb_buf,
                                  RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
                                  unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
-                                 DPConst* Ds, int gamma, double alpha, double c1d, double c2d, double c1v,
-                                 double c2v, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
+                                 int gi, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
                                  const double* best_s, double lbv)
 {
     constexpr int GL = 32 / G;
@@ -1240,15 +1323,12 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     const int gl = lane % GL;
     const unsigned gmask = G == 1 ? 0xffffffffu : (((1u << GL) - 1u) << (lane - gl));
     const int K = C.K;
-    const double L = expected_tokens(alpha, gamma);
-    const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));   // eq:step_n
+    // the per-(scenario, gamma) constants (L, N = ceil(O_max / L) by eq:ol / eq:step_n, and the
+    // Appendix-A stage-time coefficients) were computed once per scenario by solve_kernel's
+    // prologue; they stay in shared memory (all twelve in registers would spill the phase-A loop)
+    const int N = sm.nq[gi];
     const int Mx = N - 1;
-    const DPConst Dl = make_dpconst(C, gamma, L, N, c1d, c2d, c1v, c2v);
-    // the per-(scenario, gamma) constants live in shared memory: they are read
-    // once per tile, and keeping all twelve in registers spills the phase-A loop
-    if (gl == 0) *Ds = Dl;
-    __syncwarp();
-    const DPConst& D = *Ds;
+    const DPConst& D = sm.dq[gi];
     unsigned n_cand = 0, n_seg = 0, n_full = 0;
     if (gl == 0) {                           // row 0 == 0 (reading A3); empty segment pool
         *top_s = 0;
@@ -1259,7 +1339,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         rw[0].off = 0;
         rw[0].cnt = Mx >= 1 ? 1 : 0;
         rw[0].key = (R)0;
-        fence_proxy_async_global();
+        if (!RS) fence_proxy_async_global();
     }
     __syncwarp();
     int rows_done = 0;
@@ -1282,6 +1362,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
     R t_row = (R)0;                          // Upsilon[i,0,0] of the last row this lane finalized
     int jprev = 0;                           // j* of row i0-1 (the previous tile's last row)
     for (int i0 = 1; i0 <= K && !infeasible; i0 += GL) {
+        RowRec<R>* const tb = RS ? rw + i0 : tb_buf;   // the tile's GL rows
         const int i = i0 + gl;               // this lane's row
         const bool own = i <= K;
         const int jlo_i = own ? sm.jlo[i - 1] : K + 2;
@@ -1301,7 +1382,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         static_assert(kTileCh <= 32, "chunk masks are 32-bit");
         const int nrows = i0 - p0;
         const int nch = (nrows + kTileCh - 1) / kTileCh;
-        if (nch > 0) {
+        if (!RS && nch > 0) {
             const int e = min(p0 + kTileCh, i0);
 #if SDEDGE_TMA_LANE0
             if (lane == 0) bulk_load_groups<R, G>(st0, tstride, rw0, rwstride, p0, (unsigned)((e - p0) * sizeof(RowRec<R>)), 0);
@@ -1335,7 +1416,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         }
 #endif
         for (int c = 0; c < nch; ++c) {
-            if (c + 1 < nch) {
+            if (!RS && c + 1 < nch) {
                 const int a1 = p0 + (c + 1) * kTileCh, e1 = min(a1 + kTileCh, i0);
 #if SDEDGE_TMA_LANE0
                 if (lane == 0)
@@ -1347,10 +1428,12 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                               bars + ((c + 1) & 1));
 #endif
             }
-            mbar_wait(bars + (c & 1), (bar_phase >> (c & 1)) & 1u);
-            bar_phase ^= 1u << (c & 1);
+            if (!RS) {
+                mbar_wait(bars + (c & 1), (bar_phase >> (c & 1)) & 1u);
+                bar_phase ^= 1u << (c & 1);
+            }
             const int a = p0 + c * kTileCh, e = min(a + kTileCh, i0);
-            const RowRec<R>* buf = stage + (c & 1) * kTileCh;
+            const RowRec<R>* buf = RS ? rw + a : stage + (c & 1) * kTileCh;
             const double bda = (double)(i - a);
             // this lane's candidates in the chunk: predecessors max(a, pst) .. e-1
             const int lo = max(pst - a, 0), hi = e - a;
@@ -1396,7 +1479,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
 #endif
                 }
             }
-            __syncwarp();                                        // buffer (c & 1) may be refilled now
+            if (!RS) __syncwarp();                               // buffer (c & 1) may be refilled now
         }
         __syncwarp();
         // ---- phase B: the tile's rows in order.  Lane r already holds the best
@@ -1534,7 +1617,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         jprev = __shfl_sync(0xffffffffu, bj, (lane - gl) + GL - 1);
         // later tiles bulk-read this tile's rows through TMA (async proxy): every
         // lane orders the global row stores it made before the next __syncwarp
-        fence_proxy_async_global();
+        if (!RS) fence_proxy_async_global();
         __syncwarp();
 #if SDEDGE_GAMMA_ABORT
         // Exact gamma-level pruning: the optimal latency of the first i tasks is
@@ -1552,7 +1635,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             const int il = i0 + GL - 1;                          // the tile's last row
             const R kl = __shfl_sync(0xffffffffu, t_row, (lane - gl) + GL - 1);
             const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
-            const double S1 = sm.pI[K] - sm.pI[il], S2 = sm.pI2[K] - sm.pI2[il], cnt = (double)(K - il);
+            const int pt = K / kPfx + 1, pl = il / kPfx;         // il is a multiple of GL, hence of kPfx
+            const double S1 = sm.pI[pt] - sm.pI[pl], S2 = sm.pI2[pt] - sm.pI2[pl], cnt = (double)(K - il);
             const double c = D.hv2 + D.g;
             const double rest = D.kv * (S2 + (D.g + c) * S1 + cnt * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + cnt * c) +
                                 cnt * D.bvc * D.sumM;
@@ -1590,15 +1674,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
 
     // RSMEM is a template parameter so that the compiler sees shared-window
     // (32-bit, LDS/STS) addresses for the row state instead of generic ones.
-    RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)(warp * G + grp) * rows_bytes<R>(K)
+    // TILE == 2 (row store in shared memory): the in-tile pass reads the GL-row tile at rows
+    // i0 .. i0+GL-1 of the store even past row K (masked), so the store is padded to a whole tile
+    const int kPad = TILE == 2 ? rs_pad(K, GL) : 0;
+    RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)(warp * G + grp) * rows_bytes<R>(K + kPad)
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
     Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     RowRec<R>* tb = nullptr;
     RowRec<R>* stage = nullptr;
     unsigned long long* bars = nullptr;
     DPConst* dpc = nullptr;
-    if (TILE) {                              // shared tile buffer of this (warp, group) DP
-        unsigned char* t = sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K) : 0) +
+    if (TILE == 1) {                         // shared tile buffer of this (warp, group) DP
+        unsigned char* t = sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K + kPad) : 0) +
                            (size_t)(warp * G + grp) * tile_bytes<R, G>();
         tb = reinterpret_cast<RowRec<R>*>(t);
         stage = reinterpret_cast<RowRec<R>*>(t + (size_t)GL * sizeof(RowRec<R>));
@@ -1615,18 +1702,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     // warp-uniform addresses of group 0's staging buffer and row store (TMA issue)
     const unsigned tb_stride = (unsigned)tile_bytes<R, G>();
     const int wu = kWarps == 1 ? 0 : warp;
-    const unsigned st0 = TILE ? smem_u32(sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K) : 0) +
+    const unsigned st0 = TILE == 1 ? smem_u32(sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K + kPad) : 0) +
                                          (size_t)(wu * G) * tb_stride) + (unsigned)(GL * sizeof(RowRec<R>)) : 0u;
     const unsigned char* rw0 = ws.rows + (size_t)((long long)blockIdx.x * kWarps + wu) * G * C.rows_stride;
     const long long n_items = BIG ? (long long)*ws.ovf_count : n;
     short* Scta = ws.S + (size_t)blockIdx.x * (ng + 1) * K;   // this CTA's S vectors (+1: per-batch gammas)
     __shared__ bool s_ovf;
     __shared__ double s_best;                // best T_inf of the finished gammas of this scenario
-    __shared__ unsigned long long s_work[5];
+    __shared__ unsigned long long s_work[kThreads * 5];   // per-thread work counters
     __shared__ long long s_top[kWarps * G];
-    if (tid < 5) s_work[tid] = 0;
+    for (int q = 0; q < 5; ++q) s_work[tid * 5 + q] = 0;
     __syncthreads();
-    WorkCount wc{s_work};
+    WorkCount wc{out.work ? s_work + tid * 5 : nullptr};
     __shared__ double s_par[5];              // alpha, c1d, c2d, c1v, c2v of the current scenario
 
     for (;;) {
@@ -1655,7 +1742,11 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         bad = __syncthreads_or(bad);
         // ---- stable ascending sort by I_k (reading A13): bitonic sort of the unique keys
         // (I_k biased to unsigned) << 32 | k, padded to a power of two with ~0 -- O(K log^2 K / threads)
-        {
+        if (kWarps == 1 && K <= 128) {       // in registers: one warp, <= 4 keys per lane
+            if (K <= 32) warp_sort_tasks<1>(sm.I, sm.ord, sm.Is, K, lane);
+            else if (K <= 64) warp_sort_tasks<2>(sm.I, sm.ord, sm.Is, K, lane);
+            else warp_sort_tasks<4>(sm.I, sm.ord, sm.Is, K, lane);
+        } else {
             const int P2 = sort_len(K);
             for (int k = tid; k < P2; k += kThreads)
                 sm.key[k] = k < K ? ((unsigned long long)((unsigned)sm.I[k] ^ 0x80000000u) << 32) | (unsigned)k
@@ -1677,43 +1768,45 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             }
         }
         __syncthreads();
-        // prefix sums of the sorted I and I^2 (the suffix verify-work bound):
-        // each thread a contiguous chunk, then an exclusive scan of the chunk sums
+        // prefix sums of the sorted I and I^2 at rows 0, kPfx, 2 kPfx, ... and the totals (the suffix
+        // verify-work bound at tile ends): one thread per kPfx-row block, then a scan
         {
-            const int ch = (K + kThreads - 1) / kThreads, a0 = min(K, tid * ch), a1 = min(K, a0 + ch);
+            const int nb = (K + kPfx - 1) / kPfx;
             double c1 = 0.0, c2 = 0.0;
-            for (int r = a0; r < a1; ++r) { const double x = sm.Is[r]; c1 += x; c2 += x * x; }
-            if (kWarps == 1) {
+            for (int bk = tid; bk < nb; bk += kThreads)
+                for (int r = bk * kPfx; r < min(K, bk * kPfx + kPfx); ++r) {
+                    const double x = sm.Is[r];
+                    c1 += x; c2 += x * x;
+                }
+            if (kWarps == 1 && nb <= 32) {
                 double e1 = c1, e2 = c2;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const double u1 = __shfl_up_sync(0xffffffffu, e1, o), u2 = __shfl_up_sync(0xffffffffu, e2, o);
                     if (lane >= o) { e1 += u1; e2 += u2; }
                 }
-                e1 -= c1; e2 -= c2;                                  // exclusive
                 if (tid == 0) { sm.pI[0] = 0.0; sm.pI2[0] = 0.0; }
-                for (int r = a0; r < a1; ++r) {
-                    const double x = sm.Is[r];
-                    e1 += x; e2 += x * x;
-                    sm.pI[r + 1] = e1; sm.pI2[r + 1] = e2;
-                }
-            } else if (tid == 0) {
-                double e1 = 0.0, e2 = 0.0;
-                sm.pI[0] = 0.0; sm.pI2[0] = 0.0;
-                for (int r = 0; r < K; ++r) {
-                    const double x = sm.Is[r];
-                    e1 += x; e2 += x * x;
-                    sm.pI[r + 1] = e1; sm.pI2[r + 1] = e2;
+                if (tid < nb) { sm.pI[tid + 1] = e1; sm.pI2[tid + 1] = e2; }       // inclusive: row (tid+1) kPfx
+                if (tid == nb - 1) { sm.pI[K / kPfx + 1] = e1; sm.pI2[K / kPfx + 1] = e2; }   // the totals
+            } else {
+                __syncthreads();
+                if (tid == 0) {
+                    double e1 = 0.0, e2 = 0.0;
+                    sm.pI[0] = 0.0; sm.pI2[0] = 0.0;
+                    for (int r = 0; r < K; ++r) {
+                        const double x = sm.Is[r];
+                        e1 += x; e2 += x * x;
+                        if ((r + 1) % kPfx == 0) { sm.pI[(r + 1) / kPfx] = e1; sm.pI2[(r + 1) / kPfx] = e2; }
+                    }
+                    sm.pI[K / kPfx + 1] = e1; sm.pI2[K / kPfx + 1] = e2;
                 }
             }
         }
         __syncthreads();
         // ---- memory window per sorted row (gamma-independent): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
         for (int r = tid; r < K; r += kThreads) {
-            const long long room = C.gamma_s - C.Gp;
-            const long long bmax = room >= 0 ? room / (C.kvunit * ((long long)sm.Is[r] + C.O_max)) : 0;
             const int i = r + 1;
-            sm.jlo[r] = (short)(bmax >= i ? 1 : (int)(i - bmax + 1));
+            sm.jlo[r] = (short)window_lo(C.gamma_s - C.Gp, C.kvunit * ((long long)sm.Is[r] + C.O_max), i);
         }
         // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2), or the
         // uniform baseline w_k = 1/K with T_com = max_k T_k,com (eq:ul_latency)
@@ -1730,7 +1823,9 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     tc = fmax(tc, C.lambda * (double)sm.I[k] / r);
                 } else {
                     tc += C.lambda * (double)sm.I[k] / (C.Bw * sk);
-                    q += (double)sm.I[k] / sk;
+                    const double u = (double)sm.I[k] / sk;
+                    q += u;
+                    reinterpret_cast<double*>(sm.key)[k] = u;   // w*_k = u_k / sum u (the sort keys are dead)
                 }
             }
         for (int o = 16; o > 0; o >>= 1) {
@@ -1767,6 +1862,12 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         }
         __syncthreads();
         const bool bad_alpha = !(s_par[0] > 0.0 && s_par[0] < 1.0);
+        if (out.w) {                         // w* (eq:opt_w): known before any DP runs
+            double qsum = 0.0;
+            for (int w = 0; w < kWarps; ++w) qsum += sm.red[kWarps + w];
+            for (int k = tid; k < K; k += kThreads)
+                out.w[s * K + k] = bad ? dnan() : uniform ? 1.0 / K : reinterpret_cast<const double*>(sm.key)[k] / qsum;
+        }
         // (alpha and the coefficients are re-read from shared memory at each DP call:
         // nothing scenario-wide stays live in registers across the gamma loop)
 #if SDEDGE_SCEN_SMEM
@@ -1802,8 +1903,19 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 sm.dq[gi] = D;
                 sm.nq[gi] = N;
                 const double c = D.hv2 + D.g;
-                sm.glb[gi] = D.kv * (S2 + (D.g + c) * S1 + Kd * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + Kd * c) +
-                             Kd * D.bvc * D.sumM + D.c2vv * (D.Mx + 1.0);
+                const double lbv = D.kv * (S2 + (D.g + c) * S1 + Kd * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + Kd * c) +
+                                   Kd * D.bvc * D.sumM + D.c2vv * (D.Mx + 1.0);
+                // draft side: every step's makespan is at least the draft stage's
+                // serial work plus the last batch's verify time, sum_m T^d + T^v_M >= sum_k d_n(I_k)
+                // + c2d gamma + v_n(I_K) + c2v (the last batch holds task K, the longest)
+                double lbd = 0.0;
+                if (D.g > 0.0) {
+                    const double e = D.g - 1.0 + D.hd2;
+                    lbd = D.kd * (S2 + e * S1 + Kd * ((D.g - 1.0) * D.hd2 + D.tri)) +
+                          D.Mx * D.kd * (D.g * S1 + Kd * (D.g * D.hd2 + D.tri)) + Kd * D.sumM * D.bdc;
+                }
+                lbd += row_coef(D, sm.Is[K - 1]).vsl + (D.c2dg + D.c2vv) * (D.Mx + 1.0);
+                sm.glb[gi] = fmax(lbv, lbd);
                 if (one_fits) {
                     const RowCoef rc = row_coef(D, sm.Is[K - 1]);
                     one_min = fmin(one_min, Kd * (rc.td1 + rc.tv1 + D.Mx * (rc.ad + rc.av) + D.sumM * (D.bdc + D.bvc)) +
@@ -1813,14 +1925,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             for (int o = 16; o > 0; o >>= 1) one_min = fmin(one_min, __shfl_xor_sync(0xffffffffu, one_min, o));
             if (lane == 0) sm.red[4 * kWarps + warp] = one_min;
             __syncthreads();
-            for (int gi = tid; gi < ng; gi += kThreads) {
-                const double v = sm.glb[gi];
-                int r = 0;
-                for (int q2 = 0; q2 < ng; ++q2) {
-                    const double u = sm.glb[q2];
-                    r += (u < v) || (u == v && q2 < gi) || (v != v && (u == u || q2 < gi));   // NaN bounds last
+            if (warp == 0) {                 // queue: the gamma of the smallest bound first, then ascending
+                double v = dinf();
+                int a = ng;
+                for (int gi = lane; gi < ng; gi += 32)
+                    if (sm.glb[gi] < v) { v = sm.glb[gi]; a = gi; }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int oa = __shfl_xor_sync(0xffffffffu, a, o);
+                    if (ov < v || (ov == v && oa < a)) { v = ov; a = oa; }
                 }
-                sm.gord[r] = gi;
+                if (a >= ng) a = 0;                                  // all bounds NaN / inf
+                for (int pos = lane; pos < ng; pos += 32) sm.gord[pos] = pos == 0 ? a : (pos <= a ? pos - 1 : pos);
             }
             if (tid == 0) {
                 double m = dinf();
@@ -1843,13 +1959,34 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 }
             }
         } else if (!bad && !bad_alpha) {
+            // exact gamma-level pruning before the first row, for the proposed
+            // policy: a gamma whose lower bound exceeds the best finished (or seeded) T_inf can
+            // neither win nor tie -- it is dropped from the queue without a DP call
+            const bool prune = SDEDGE_GAMMA_ABORT && mono && C.batch_policy == SDEDGE_BATCH_PROPOSED;
+            const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
             for (;;) {
-                int gi0 = 0;
-                if (lane == 0) gi0 = atomicAdd(&sm.ctl[0], G);
-                gi0 = __shfl_sync(0xffffffffu, gi0, 0);
-                if (gi0 >= ng) break;
-                const bool active = gi0 + grp < ng;  // an idle group repeats gi0 without writing
-                const int gi = sm.gord[active ? gi0 + grp : gi0];   // queue position -> gamma index
+                // lane 0 takes the next G unpruned gammas of the queue (most promising first)
+                int mine = -1;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    int sel = -1;
+                    if (lane == 0)
+                        for (;;) {
+                            const int pos = atomicAdd(&sm.ctl[0], 1);
+                            if (pos >= ng) break;
+                            const int q = sm.gord[pos];
+                            if (prune && sm.glb[q] * (1.0 - mg) > s_best * (1.0 + mg)) { sm.tinf[q] = dinf(); continue; }
+                            sel = q;
+                            break;
+                        }
+                    sel = __shfl_sync(0xffffffffu, sel, 0);
+                    if (g == grp) mine = sel;
+                    if (g == 0 && sel < 0) break;
+                }
+                const int first = __shfl_sync(0xffffffffu, mine, 0);
+                if (first < 0) break;
+                const bool active = mine >= 0;       // an idle group repeats the first gamma without writing
+                const int gi = active ? mine : first;
                 bool ovf = false;
                 short* Sg = active ? Scta + (size_t)gi * K : nullptr;
                 const short* jf = (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX)
@@ -1859,8 +1996,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 // other instantiations compile just their own DP (fewer live registers)
                 constexpr bool kBase = G == 1 && !TILE;
                 if constexpr (TILE) {
-                    t = dp_gamma_tiled<R, G>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
-                                             C.rows_stride, dpc, C.gmin + gi, SDEDGE_SCEN_ARGS,
+                    t = dp_gamma_tiled<R, G, TILE == 2>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
+                                             C.rows_stride, gi,
                                              Sg, &ovf, wc, &s_top[warp * G + grp], active,
                                              (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr, sm.glb[gi]);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
@@ -1876,7 +2013,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     };
                     double tb = dinf();
                     int bb = 1;
-                    for (int b = K >= 2 ? 2 : 1; b <= K; ++b) {
+                    const int b0 = (C.flags & SDEDGE_FLAG_HEURISTIC_HALF) ? (K + 1) / 2 : (K >= 2 ? 2 : 1);
+                    for (int b = b0; b <= K; ++b) {
                         plan(b);
                         const double tt = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS,
                                                                nullptr, &ovf, wc, &s_top[warp * G + grp],
@@ -1891,17 +2029,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
                                              &s_top[warp * G + grp], active, jw);
                 } else {
-                    // exact gamma-level pruning before the first row, for the
-                    // proposed policy: a gamma whose lower bound exceeds the best finished (or
-                    // seeded) T_inf cannot win or tie; the call is skipped when every group's can't
-                    bool skip = false;
-                    if (SDEDGE_GAMMA_ABORT && mono && C.batch_policy == SDEDGE_BATCH_PROPOSED) {
-                        const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
-                        skip = __all_sync(0xffffffffu, !active || sm.glb[gi] * (1.0 - mg) > s_best * (1.0 + mg));
-                    }
-                    t = skip ? dinf()
-                             : dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
-                                                    &s_top[warp * G + grp], active, kBase ? jf : nullptr);
+                    t = dp_gamma<R, ALGO, G>(C, sm, rw, pl, C.gmin + gi, SDEDGE_SCEN_ARGS, Sg, &ovf, wc,
+                                             &s_top[warp * G + grp], active, kBase ? jf : nullptr);
                 }
                 if (lane % GL == 0 && active) {
                     sm.tinf[gi] = t;
@@ -1954,7 +2083,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (st == 0) {
                 const short* S = Scta + (size_t)gbest * K;
                 int i = K;
-                while (i > 0) { sm.I[M++] = i; i = S[i - 1] - 1; }   // reuse sm.I as a stack
+                int* stk = reinterpret_cast<int*>(sm.key);          // the sort keys are dead: a stack
+                while (i > 0) { stk[M++] = i; i = S[i - 1] - 1; }
                 lat[0] = Tcom + best; lat[1] = Tcom; lat[2] = best;
                 out.gamma[s] = pbg ? (int)Scta[(size_t)ng * K + K - 1] : C.gmin + gbest;   // pbg: the last batch's
             } else {
@@ -1973,30 +2103,26 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         const int M = sm.ctl[2];
         for (int k = tid; k < K; k += kThreads) {
             out.order[s * K + k] = sm.ord[k];
-            out.bend[s * K + k] = k < M ? sm.I[M - 1 - k] : 0;
+            out.bend[s * K + k] = k < M ? reinterpret_cast<const int*>(sm.key)[M - 1 - k] : 0;
         }
         if (out.bgam)                        // each batch's gamma (gamma* for all unless per-batch)
             for (int k = tid; k < K; k += kThreads)
-                out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + sm.I[M - 1 - k] - 1]
+                out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + reinterpret_cast<const int*>(sm.key)[M - 1 - k] - 1]
                                                        : C.gmin + sm.ctl[4];
         if (out.trace) {                     // S vector of gamma* (row choices; 0 unless status 0)
             const short* S = Scta + (size_t)max(sm.ctl[4], 0) * K;
             for (int k = tid; k < K; k += kThreads) out.trace[s * K + k] = M > 0 ? (int32_t)S[k] : 0;
         }
-        if (out.w)
-            for (int k = tid; k < K; k += kThreads) {
-                double wk = dnan();
-                if (!sm.ctl[3]) {
-                    const double sk = log2(1.0 + in.p[s * K + k] * in.g[s * K + k] / C.sigma2);
-                    wk = C.bw_policy == SDEDGE_BW_UNIFORM ? 1.0 / K : ((double)in.I[s * K + k] / sk) / qsum;
-                }
-                out.w[s * K + k] = wk;
-            }
+
         __syncthreads();
     }
     if (out.work) {
         __syncthreads();
-        if (tid < 5) atomicAdd(out.work + tid, s_work[tid]);
+        if (tid < 5) {
+            unsigned long long v = 0;
+            for (int t = 0; t < kThreads; ++t) v += s_work[t * 5 + tid];
+            atomicAdd(out.work + tid, v);
+        }
     }
 }
 
@@ -2382,7 +2508,7 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
     if (p->mem_capacity_bytes < 0) return fail(-1, "mem_capacity_bytes < 0");
     if (p->precision != 0 && p->precision != 1) return fail(-1, "precision must be 0 (fp64) or 1 (fp32)");
     if (p->algo != SDEDGE_ALGO_ENVELOPE && p->algo != SDEDGE_ALGO_DENSE) return fail(-1, "unknown algo");
-    if (p->flags & ~SDEDGE_FLAG_TINY_POOL) return fail(-1, "unknown flags");
+    if (p->flags & ~(SDEDGE_FLAG_TINY_POOL | SDEDGE_FLAG_HEURISTIC_HALF)) return fail(-1, "unknown flags");
     if (p->bandwidth_policy != SDEDGE_BW_OPTIMAL && p->bandwidth_policy != SDEDGE_BW_UNIFORM)
         return fail(-1, "unknown bandwidth_policy");
     if (p->batching_policy < SDEDGE_BATCH_PROPOSED || p->batching_policy > SDEDGE_BATCH_PER_BATCH_GAMMA)
@@ -2459,14 +2585,15 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     Consts C = C0;
     const size_t rb = rows_bytes<R>(C.K);
     // row state in shared memory when it keeps >= 3 CTAs (12 warps) per SM
-    C.rows_in_smem = !TILE && smem_bytes<R, G>(C.K, C.ng, 1, 0) <= (size_t)(220 * 1024 / 3) ? 1 : 0;
-    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE);
+    // row state in shared memory when it keeps >= 3 CTAs per SM (untiled), always for TILE == 2
+    C.rows_in_smem = TILE == 2 ? 1 : (!TILE && smem_bytes<R, G>(C.K, C.ng, 1, 0) <= (size_t)(220 * 1024 / 3) ? 1 : 0);
+    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE == 1, TILE == 2 ? rs_pad(C.K, 32 / G) : 0);
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
     // (the tiled DP keeps its rows in global memory: no RSMEM instantiation for it)
-    auto k_main = (!TILE && C.rows_in_smem) ? solve_kernel<R, ALGO, TILE ? 0 : 1, G, TILE>
-                                            : solve_kernel<R, ALGO, 0, G, TILE>;
+    auto k_main = (TILE != 1 && C.rows_in_smem) ? solve_kernel<R, ALGO, TILE == 1 ? 0 : 1, G, TILE>
+                                                : solve_kernel<R, ALGO, 0, G, TILE>;
     auto k_big = k_main;
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
@@ -2545,6 +2672,7 @@ Consts make_consts(const sdedge_params* p)
     C.bw_policy = p->bandwidth_policy;
     C.batch_policy = p->batching_policy;
     C.static_batch = p->static_batch;
+    C.flags = p->flags;
     return C;
 }
 
@@ -2562,16 +2690,20 @@ int solve_device(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, d
     const int f = p->flags;
     const bool base = p->algo == SDEDGE_ALGO_DENSE || p->batching_policy != SDEDGE_BATCH_PROPOSED;
     const bool tiled = !base && p->K > SDEDGE_TILE_MIN_K;
+    // tiled DP with the row store in shared memory (no TMA staging) while it stays small
+    const bool rs = tiled && p->K <= SDEDGE_RS_MAX_K;
     const int G = base ? 1 : (p->K <= 48 ? 4 : 2);
     if (p->precision == 0) {
         if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<double, SDEDGE_ALGO_DENSE, 1, 0>(C, in, out, n, st, f);
         if (base) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 1, 0>(C, in, out, n, st, f);
+        if (rs) return launch_all<double, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 2>(C, in, out, n, st, f);
         if (tiled) return launch_all<double, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 1>(C, in, out, n, st, f);
         if (G == 4) return launch_all<double, SDEDGE_ALGO_ENVELOPE, 4, 0>(C, in, out, n, st, f);
         return launch_all<double, SDEDGE_ALGO_ENVELOPE, 2, 0>(C, in, out, n, st, f);
     }
     if (p->algo == SDEDGE_ALGO_DENSE) return launch_all<float, SDEDGE_ALGO_DENSE, 1, 0>(C, in, out, n, st, f);
     if (base) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 1, 0>(C, in, out, n, st, f);
+    if (rs) return launch_all<float, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 2>(C, in, out, n, st, f);
     if (tiled) return launch_all<float, SDEDGE_ALGO_ENVELOPE, SDEDGE_TILE_G, 1>(C, in, out, n, st, f);
     if (G == 4) return launch_all<float, SDEDGE_ALGO_ENVELOPE, 4, 0>(C, in, out, n, st, f);
     return launch_all<float, SDEDGE_ALGO_ENVELOPE, 2, 0>(C, in, out, n, st, f);

@@ -38,7 +38,7 @@ def test_struct_layout_matches_header():
 @pytest.mark.parametrize("bad", [dict(K=0), dict(K=1025), dict(gamma_min=3, gamma_max=2),
                                  dict(gamma_max=65), dict(O_max=0), dict(noise_w=0.0),
                                  dict(bandwidth_hz=-1.0), dict(c1_draft=float("nan")),
-                                 dict(precision=2), dict(algo=7), dict(flags=2), dict(draft=(0, 768, 3072)),
+                                 dict(precision=2), dict(algo=7), dict(flags=4), dict(draft=(0, 768, 3072)),
                                  dict(verify=(32, 70000, 11008)), dict(downlink_s=-1.0),
                                  dict(bandwidth_policy=2), dict(batching_policy=7),
                                  dict(batching_policy=3, static_batch=0)])

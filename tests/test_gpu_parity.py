@@ -303,17 +303,21 @@ def test_host_entry_point_chunked():
 
 
 # ---------------------------------------------------------------- paper baselines (NEXT-2)
-@pytest.mark.parametrize("pol", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("pol", [1, 2, 3, 4, 5, "5half"])
 def test_batching_policies(pol):
-    """SD w/o pipeline, no batching, static, max and heuristic batching
-     against the oracle."""
+    """SD w/o pipeline, no batching, static, max and heuristic batching (both
+    readings B5 and B5') against the oracle."""
     _, sc, _ = scengen.config("C3", 0, 300)
+    hs = 1 if pol == "5half" else 0
+    pol = 5 if pol == "5half" else pol
     for pair in ("68M-7B", "1.1B-7B"):
-        pd = dict(scengen.params(pair, K=32, gamma_min=1, gamma_max=8), batching_policy=pol, static_batch=5)
+        pd = dict(scengen.params(pair, K=32, gamma_min=1, gamma_max=8), batching_policy=pol, static_batch=5,
+                  heuristic_start=hs)
         for algo in (ENV, DENSE):
             res, _, g = _check(pd, sc, 0, algo)
             assert res["failures"] == 0
-    pd = dict(scengen.params("1.1B-7B", K=128, gamma_min=1, gamma_max=16), batching_policy=pol, static_batch=5)
+    pd = dict(scengen.params("1.1B-7B", K=128, gamma_min=1, gamma_max=16), batching_policy=pol, static_batch=5,
+              heuristic_start=hs)
     _, sc4, _ = scengen.config("C4", 0, 24)
     _check(pd, sc4, 0, ENV)
 

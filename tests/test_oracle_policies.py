@@ -113,6 +113,27 @@ def test_heuristic_stopping_rule(orc):
         assert ends == plan(b)
 
 
+def test_heuristic_from_two_batches(orc):
+    """Reading B5': start from two batches, b = ceil(K/2), and grow b
+    while eq:time keeps improving -- checked against eval_plan of every plan."""
+    rng = np.random.default_rng(37)
+    for _ in range(25):
+        K = int(rng.integers(2, 24))
+        pd = dict(scengen.params("1.1B-7B", K=K, O_max=int(rng.choice([64, 512]))), batching_policy=HEUR,
+                  heuristic_start=1)
+        Is = np.sort(rng.integers(1, 513, K)).astype(np.int32)
+        a = float(rng.uniform(0.5, 0.9))
+        g = int(rng.integers(1, 9))
+
+        def plan(b):
+            return [e for e in range(b, K, b)] + [K]
+        b = (K + 1) // 2
+        T = {q: orc.eval_plan(pd, Is, a, g, plan(q)) for q in range(b, K + 1)}
+        while b + 1 <= K and T[b + 1] < T[b]:
+            b += 1
+        assert orc.fixed_plan(pd, Is, a, g) == plan(b)
+
+
 def test_policy_solves_are_consistent(orc):
     """Every policy's T_inf equals the literal evaluation of its own plan and
     gamma; FSL is gamma_min = gamma_max = 7; ADS core is gamma = 0."""
@@ -264,3 +285,35 @@ def test_row_value_plus_remaining_verify_work(orc, pair):
                 n_tight += bound > 0.9 * t
             assert np.all(np.diff(rt) >= vsl[1:] * (1 - 1e-12) - 1e-12 * rt[1:])   # row by row
     assert n_tight > 0
+
+
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B", "1.1B-13B"])
+def test_t_inf_at_least_draft_work(orc, pair):
+    """T_inf(gamma) >= sum_k dsl(I_k) + vsl(I_K) + (gamma c2d + c2v) N: every step's
+    makespan (eq:time) is at least the draft stage's serial work -- each batch's
+    draft time is affine in its size with a slope growing with the padded length
+    (eq:flops_d, eq:latency_b2, eq:d_latency), so each task pays at least its own
+    length's slope and some batch the intercept -- plus the last batch's verify
+    time, which holds task K.  The GPU uses max(this, the verify-side bound) to
+    skip a gamma before its DP; pinned on the literal DP."""
+    K = 10
+    pd = scengen.params(pair, K=K, gamma_min=1, gamma_max=8, O_max=160)
+    sc = scengen.generate(95, K, 0, 5)
+    n_tight = 0
+    for s in range(5):
+        Is = np.sort(sc["I"][s])
+        alpha = float(sc["alpha"][s])
+        for gamma in (1, 3, 6):
+            L = orc.expected_tokens(alpha, gamma)
+            N = orc.decode_steps(pd["O_max"], L)
+            t_inf = orc.dp(pd, Is, alpha, gamma)[0]
+            lb = 0.0
+            for n in range(1, N + 1):
+                for I in Is:
+                    lb += orc.draft_time(pd, 2, int(I), gamma, L, n) - orc.draft_time(pd, 1, int(I), gamma, L, n)
+                d1 = orc.draft_time(pd, 1, int(Is[-1]), gamma, L, n)
+                lb += 2 * d1 - orc.draft_time(pd, 2, int(Is[-1]), gamma, L, n)      # one draft intercept
+                lb += orc.verify_time(pd, 1, int(Is[-1]), gamma, L, n)              # last batch's verify
+            assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
+            n_tight += lb > 0.6 * t_inf
+    assert n_tight > 0 or pair == "68M-7B"
