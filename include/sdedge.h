@@ -221,6 +221,15 @@ int sdedge_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
 int sdedge_ipc_open(const void* handle, uint64_t offset, void** dev_ptr);
 int sdedge_ipc_close(void* dev_ptr, uint64_t offset);
 
+/* Per-kernel timing for measurement (bench.py's roofline): sdedge_kernel_timing(1) clears the
+ * record and starts bracketing every launch the solve calls on this thread enqueue with CUDA
+ * events on the launch's own stream (0 stops).  sdedge_kernel_times waits for the recorded
+ * events and writes the summed milliseconds per kernel kind to ms[4] -- [0] the prep kernel of
+ * the tiled path, [1] the main DP launch, [2] the worst-case-pool pass, [3] other -- and the
+ * launch counts to launches[4] (optional).  At most 4096 launches are recorded. */
+int sdedge_kernel_timing(int32_t enable);
+int sdedge_kernel_times(double* ms, int32_t* launches);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int sdedge_last_launch_count(void);
 

@@ -23,7 +23,7 @@ FLAG_TINY_POOL, FLAG_HEURISTIC_HALF = 1, 2
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
                     "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
                     "sdedge_abi_version", "sdedge_pipe_peak", "sdedge_ipc_export", "sdedge_ipc_open",
-                    "sdedge_ipc_close")
+                    "sdedge_ipc_close", "sdedge_kernel_timing", "sdedge_kernel_times")
 
 
 class SdedgeModel(C.Structure):
@@ -84,6 +84,10 @@ def lib() -> C.CDLL:
         L.sdedge_ipc_open.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
         L.sdedge_ipc_close.restype = C.c_int
         L.sdedge_ipc_close.argtypes = [C.c_void_p, C.c_uint64]
+        L.sdedge_kernel_timing.restype = C.c_int
+        L.sdedge_kernel_timing.argtypes = [C.c_int32]
+        L.sdedge_kernel_times.restype = C.c_int
+        L.sdedge_kernel_times.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.sdedge_pipe_peak.restype = C.c_int
         L.sdedge_pipe_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib = L
@@ -235,6 +239,21 @@ def brute_force(params: dict, I, alpha, coeffs=None, stream=None, work_counters=
     sdedge_brute_force(I, alpha, coeffs, n, P, o["t_inf"], o["gamma"], o["M"], o["batch_end"], o["order"],
                        o["status"], work_counters)
     return o
+
+
+def sdedge_kernel_timing(enable: bool) -> None:
+    lib().sdedge_kernel_timing(1 if enable else 0)
+
+
+def sdedge_kernel_times() -> dict:
+    """Summed ms and launch counts per kernel kind since sdedge_kernel_timing(True)."""
+    ms = (C.c_double * 4)()
+    cnt = (C.c_int32 * 4)()
+    rc = lib().sdedge_kernel_times(ms, cnt)
+    if rc != 0:
+        raise RuntimeError(f"sdedge_kernel_times failed ({rc}): {sdedge_last_error()}")
+    names = ("prep", "main", "big", "other")
+    return {names[k]: (ms[k], cnt[k]) for k in range(4)}
 
 
 def sdedge_pipe_peak(fp32: bool = False):

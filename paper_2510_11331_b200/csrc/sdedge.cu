@@ -36,6 +36,41 @@ namespace {
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
 
+// Optional per-kernel timing (sdedge_kernel_timing): while enabled, every launch of the solve is
+// bracketed by CUDA events on its own stream; sdedge_kernel_times sums the durations per kernel
+// kind.  Events are recycled, so a long timed region costs no allocation after the first steps.
+struct KTiming {
+    bool on = false;
+    int used = 0;
+    int kind[4096];
+    cudaEvent_t ev[4096][2];
+    int created = 0;
+};
+thread_local KTiming g_kt;
+
+enum { KT_PREP = 0, KT_MAIN = 1, KT_BIG = 2, KT_OTHER = 3 };
+
+inline int kt_begin(int kind, cudaStream_t st)
+{
+    if (!g_kt.on || g_kt.used >= 4096) return -1;
+    const int q = g_kt.used++;
+    if (q >= g_kt.created) {
+        if (cudaEventCreate(&g_kt.ev[q][0]) != cudaSuccess || cudaEventCreate(&g_kt.ev[q][1]) != cudaSuccess) {
+            --g_kt.used;
+            return -1;
+        }
+        g_kt.created = q + 1;
+    }
+    g_kt.kind[q] = kind;
+    cudaEventRecord(g_kt.ev[q][0], st);
+    return q;
+}
+
+inline void kt_end(int q, cudaStream_t st)
+{
+    if (q >= 0) cudaEventRecord(g_kt.ev[q][1], st);
+}
+
 int fail(int code, const char* msg)
 {
     snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -51,6 +86,9 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #endif
 #ifndef SDEDGE_TILE_SHFL_ARGMIN
 #define SDEDGE_TILE_SHFL_ARGMIN 1
+#endif
+#ifndef SDEDGE_POOL_SMEM
+#define SDEDGE_POOL_SMEM 1    // allow the first-pass envelope pool in shared memory (draft-bound pairs)
 #endif
 #ifndef SDEDGE_RS_MAX_K
 #define SDEDGE_RS_MAX_K 160   // tiled DP keeps its row store in shared memory up to this K
@@ -77,6 +115,9 @@ struct Consts {
     long long pool_cap;                  // envelope segments per warp slot
     long long rows_stride;               // bytes of one warp's global row state
     long long ybuf_stride;               // doubles of one CTA's per-batch-gamma rows, (K+1) x 2 x O_max
+    long long prep_stride;               // bytes of one scenario's prep record (two-kernel path)
+    int pool_smem;                       // first-pass envelope pool in shared memory (TILE == 2)
+    long long pool_cap_smem;             // its capacity in segments
 };
 
 struct Inputs {
@@ -123,7 +164,8 @@ __device__ inline void work_flush(const WorkCount& wc, bool active, unsigned can
 
 struct Work {
     short* S;                      // [grid][ng][K] boundaries j* (1-based), one block per CTA
-    unsigned long long* next;      // [2] scenario queue heads (main, big)
+    unsigned long long* next;      // [3] scenario queue heads (main, big, prep)
+    unsigned char* prep;           // [n] prep records of C.prep_stride bytes (two-kernel path)
     unsigned int* ovf_count;       // scenarios handed to the big-pool pass
     long long* ovf_list;           // [n]
     unsigned char* rows;           // global row state (when not in smem)
@@ -438,6 +480,8 @@ __device__ inline DPConst make_dpconst(const Consts& C, int gamma, double L, int
 // b <= bmax = floor(room / d) tasks fit, room = Gamma_s - Gamma_p, d = 4 Jd hd (I + O_max).
 // Exact integer floor; below 2^52 it is a double division (correctly rounded, so at most one
 // too high) with an exact integer fix-up instead of a 64-bit integer division.
+__device__ __noinline__ long long div_slow(long long a, long long b) { return a / b; }
+
 __device__ inline int window_lo(long long room, long long d, int i)
 {
     long long bmax = 0;
@@ -446,7 +490,7 @@ __device__ inline int window_lo(long long room, long long d, int i)
             bmax = (long long)((double)room / (double)d);
             if (bmax * d > room) --bmax;
         } else {
-            bmax = room / d;
+            bmax = div_slow(room, d);
         }
     }
     return bmax >= i ? 1 : (int)(i - bmax + 1);
@@ -459,9 +503,9 @@ template <int E>
 __device__ inline void warp_bitonic(unsigned long long (&x)[E], int lane)
 {
     constexpr int P = 32 * E;
-#pragma unroll
+#pragma unroll 1
     for (int sz = 2; sz <= P; sz <<= 1) {
-#pragma unroll
+#pragma unroll 1
         for (int st = sz >> 1; st > 0; st >>= 1) {
             if (st >= E) {
 #pragma unroll
@@ -471,12 +515,16 @@ __device__ inline void warp_bitonic(unsigned long long (&x)[E], int lane)
                     const bool keep_min = ((e & sz) == 0) == ((e & st) == 0);   // ascending half's lower element
                     x[r] = keep_min ? (o < x[r] ? o : x[r]) : (o > x[r] ? o : x[r]);
                 }
-            } else {
+            } else {                         // st < E: pairs (r, r + st) inside the lane
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    if (r & st) continue;
-                    const unsigned long long a = x[r], b = x[r | st];
-                    if ((a > b) == (((lane * E + r) & sz) == 0)) { x[r] = b; x[r | st] = a; }
+                for (int sv = 1; sv < E; sv <<= 1) {   // constant register indices
+                    if (st != sv) continue;
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        if (r & sv) continue;
+                        const unsigned long long a = x[r], b = x[r | sv];
+                        if ((a > b) == (((lane * E + r) & sz) == 0)) { x[r] = b; x[r | sv] = a; }
+                    }
                 }
             }
         }
@@ -604,6 +652,52 @@ __device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
     b = (b + 15) & ~(size_t)15;
     s.rows = base + b;
     return s;
+}
+
+// ------------------------------------------------------------ prep records (two-kernel hot path)
+// The tiled hot path runs as two kernels: PHASE 1 (prep: staging, sort, windows, bandwidth, w*,
+// prefix sums, per-gamma bounds; writes order, w*, T_com and every output of an invalid
+// scenario) and PHASE 2 (the DPs and the backtrack).  Each kernel's code is small enough for the
+// instruction caches, and every warp of an SM runs the same phase.  Per scenario the prep record
+// carries what PHASE 2 needs:
+struct PrepView {
+    int* Is;       // [K] sorted lengths
+    short* jlo;    // [K] first feasible j per row
+    double* pI;    // [pfx_len(K)] prefix sums of I (at every kPfx-th row, then the total)
+    double* pI2;   // [pfx_len(K)] ... of I^2
+    double* glb;   // [ng] lower bound of T_inf(gamma)
+    double* L;     // [ng] expected tokens per step (eq:ol)
+    int* N;        // [ng] decoding steps (eq:step_n)
+    double* misc;  // [2] seed of the best T_inf (min single-batch latency), T_com
+    int* flags;    // [1] bit 0 bad task, bit 1 bad alpha, bit 2 monotone coefficients
+};
+
+__host__ __device__ inline size_t prep_stride(int K, int ng)
+{
+    size_t b = 0;
+    b += ((size_t)K * 4 + 7) & ~(size_t)7;
+    b += ((size_t)K * 2 + 7) & ~(size_t)7;
+    b += 2 * (size_t)pfx_len(K) * 8;
+    b += (size_t)ng * 16;
+    b += ((size_t)ng * 4 + 7) & ~(size_t)7;
+    b += 16 + 8;
+    return (b + 15) & ~(size_t)15;
+}
+
+__device__ inline PrepView prep_view(unsigned char* base, int K, int ng)
+{
+    PrepView v;
+    size_t b = 0;
+    v.Is = reinterpret_cast<int*>(base + b); b += ((size_t)K * 4 + 7) & ~(size_t)7;
+    v.jlo = reinterpret_cast<short*>(base + b); b += ((size_t)K * 2 + 7) & ~(size_t)7;
+    v.pI = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * 8;
+    v.pI2 = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * 8;
+    v.glb = reinterpret_cast<double*>(base + b); b += (size_t)ng * 8;
+    v.L = reinterpret_cast<double*>(base + b); b += (size_t)ng * 8;
+    v.N = reinterpret_cast<int*>(base + b); b += ((size_t)ng * 4 + 7) & ~(size_t)7;
+    v.misc = reinterpret_cast<double*>(base + b); b += 16;
+    v.flags = reinterpret_cast<int*>(base + b);
+    return v;
 }
 
 // ------------------------------------------------------------ envelope update
@@ -1660,10 +1754,14 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
 #define SDEDGE_MINB 16    // min resident CTAs per SM requested from ptxas (128-register cap)
 #endif
 
-template <typename R, int ALGO, int RSMEM, int G, int TILE>
-__global__ void __launch_bounds__(kThreads, SDEDGE_MINB)
+#ifndef SDEDGE_MINB_PREP
+#define SDEDGE_MINB_PREP 32   // the prep kernel (PHASE 1): 64 registers, 32 one-warp CTAs per SM
+#endif
+template <typename R, int ALGO, int RSMEM, int G, int TILE, int PHASE>
+__global__ void __launch_bounds__(kThreads, PHASE == 1 ? SDEDGE_MINB_PREP : SDEDGE_MINB)
 solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Work ws, int BIG)
 {
+    static_assert(PHASE == 0 || (TILE != 0 && kWarps == 1), "the two-kernel path is the tiled, one-warp CTA");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = C.K, ng = C.ng;
     const Smem sm = carve_smem(smem_raw, K, ng);
@@ -1679,12 +1777,16 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     const int kPad = TILE == 2 ? rs_pad(K, GL) : 0;
     RowRec<R>* rw = carve_rows<R>(RSMEM ? sm.rows + (size_t)(warp * G + grp) * rows_bytes<R>(K + kPad)
                                      : ws.rows + (size_t)slot * C.rows_stride, K);
-    Pool<R> pl = carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
+    // first-pass envelope pool: shared memory after the row store when C.pool_smem (TILE == 2, one DP
+    // per CTA), else this slot's block of the global pool; the worst-case pass (BIG) is always global
+    const bool pool_s = TILE == 2 && PHASE == 2 && C.pool_smem && !BIG;
+    Pool<R> pl = pool_s ? carve_pool<R>(sm.rows + (size_t)kWarps * G * rows_bytes<R>(K + kPad), C.pool_cap_smem)
+                        : carve_pool<R>(ws.pool + (size_t)slot * pool_bytes<R>(C.pool_cap), C.pool_cap);
     RowRec<R>* tb = nullptr;
     RowRec<R>* stage = nullptr;
     unsigned long long* bars = nullptr;
     DPConst* dpc = nullptr;
-    if (TILE == 1) {                         // shared tile buffer of this (warp, group) DP
+    if (TILE == 1 && PHASE != 1) {           // shared tile buffer of this (warp, group) DP (none in prep)
         unsigned char* t = sm.rows + (RSMEM ? (size_t)kWarps * G * rows_bytes<R>(K + kPad) : 0) +
                            (size_t)(warp * G + grp) * tile_bytes<R, G>();
         tb = reinterpret_cast<RowRec<R>*>(t);
@@ -1718,7 +1820,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
 
     for (;;) {
         if (tid == 0) {
-            const unsigned long long it = atomicAdd(ws.next + BIG, 1ULL);
+            const unsigned long long it = atomicAdd(ws.next + (PHASE == 1 ? 2 : BIG), 1ULL);
             sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
             sm.ctl[0] = 0;
             s_ovf = false;
@@ -1728,11 +1830,16 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         const long long s = sm.sid[0];
         if (s < 0) break;
 
+        int bad = 0;
+        const bool uniform = C.bw_policy == SDEDGE_BW_UNIFORM;
+        bool bad_alpha = false, mono = true;
+        double Tcom = 0.0;
+        if constexpr (PHASE != 2) {
         // ---- stage + validate (SoA, coalesced)
         const int32_t* Ig = in.I + s * K;
         const double* pg = in.p + s * K;
         const double* gg = in.g + s * K;
-        int bad = 0;
+        #pragma unroll 1
         for (int k = tid; k < K; k += kThreads) {
             const int Ik = Ig[k];
             const double pk = pg[k], gk = gg[k];
@@ -1742,10 +1849,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         bad = __syncthreads_or(bad);
         // ---- stable ascending sort by I_k (reading A13): bitonic sort of the unique keys
         // (I_k biased to unsigned) << 32 | k, padded to a power of two with ~0 -- O(K log^2 K / threads)
-        if (kWarps == 1 && K <= 128) {       // in registers: one warp, <= 4 keys per lane
-            if (K <= 32) warp_sort_tasks<1>(sm.I, sm.ord, sm.Is, K, lane);
-            else if (K <= 64) warp_sort_tasks<2>(sm.I, sm.ord, sm.Is, K, lane);
-            else warp_sort_tasks<4>(sm.I, sm.ord, sm.Is, K, lane);
+        if (kWarps == 1 && K <= 128) {       // in registers: one warp, 4 keys per lane
+            warp_sort_tasks<4>(sm.I, sm.ord, sm.Is, K, lane);
         } else {
             const int P2 = sort_len(K);
             for (int k = tid; k < P2; k += kThreads)
@@ -1761,6 +1866,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     }
                     block_sync();
                 }
+            #pragma unroll 1
             for (int r = tid; r < K; r += kThreads) {
                 const int k = (int)(unsigned)(sm.key[r] & 0xffffffffULL);
                 sm.ord[r] = k;
@@ -1773,6 +1879,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         {
             const int nb = (K + kPfx - 1) / kPfx;
             double c1 = 0.0, c2 = 0.0;
+            #pragma unroll 1
             for (int bk = tid; bk < nb; bk += kThreads)
                 for (int r = bk * kPfx; r < min(K, bk * kPfx + kPfx); ++r) {
                     const double x = sm.Is[r];
@@ -1793,6 +1900,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 if (tid == 0) {
                     double e1 = 0.0, e2 = 0.0;
                     sm.pI[0] = 0.0; sm.pI2[0] = 0.0;
+                    #pragma unroll 1
                     for (int r = 0; r < K; ++r) {
                         const double x = sm.Is[r];
                         e1 += x; e2 += x * x;
@@ -1804,15 +1912,16 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         }
         __syncthreads();
         // ---- memory window per sorted row (gamma-independent): b <= floor((Gs - Gp) / (4 Jd hd (I + O)))
+        #pragma unroll 1
         for (int r = tid; r < K; r += kThreads) {
             const int i = r + 1;
             sm.jlo[r] = (short)window_lo(C.gamma_s - C.Gp, C.kvunit * ((long long)sm.Is[r] + C.O_max), i);
         }
         // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2), or the
         // uniform baseline w_k = 1/K with T_com = max_k T_k,com (eq:ul_latency)
-        const bool uniform = C.bw_policy == SDEDGE_BW_UNIFORM;
         double tc = 0.0, q = 0.0, s1 = 0.0, s2 = 0.0;   // s1, s2: sum I_k, sum I_k^2 (exact integers)
         if (!bad)
+            #pragma unroll 1
             for (int k = tid; k < K; k += kThreads) {
                 const double Ikd = (double)sm.I[k];
                 s1 += Ikd;
@@ -1840,13 +1949,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             sm.red[2 * kWarps + warp] = s1; sm.red[3 * kWarps + warp] = s2;
         }
         // ---- fixed-plan baselines (gamma-independent): start of the batch ending at each row
-        if (C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX) {
+        if (!TILE && C.batch_policy >= SDEDGE_BATCH_NONE && C.batch_policy <= SDEDGE_BATCH_MAX) {
             int b = 1;
             if (C.batch_policy == SDEDGE_BATCH_STATIC) b = min(C.static_batch, K);
             if (C.batch_policy == SDEDGE_BATCH_MAX) {      // largest size for the longest input (reading B4)
                 const int jl = sm.jlo[K - 1];
                 b = jl > K ? 0 : K - jl + 1;
             }
+            #pragma unroll 1
             for (int r = tid; r < K; r += kThreads) {
                 const int e = r + 1;
                 sm.jf[r] = b < 1 ? (short)(e == K ? -1 : 0)
@@ -1861,10 +1971,11 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             s_par[4] = in.coeffs ? in.coeffs[4 * s + 3] : C.c2v;
         }
         __syncthreads();
-        const bool bad_alpha = !(s_par[0] > 0.0 && s_par[0] < 1.0);
+        bad_alpha = !(s_par[0] > 0.0 && s_par[0] < 1.0);
         if (out.w) {                         // w* (eq:opt_w): known before any DP runs
             double qsum = 0.0;
             for (int w = 0; w < kWarps; ++w) qsum += sm.red[kWarps + w];
+            #pragma unroll 1
             for (int k = tid; k < K; k += kThreads)
                 out.w[s * K + k] = bad ? dnan() : uniform ? 1.0 / K : reinterpret_cast<const double*>(sm.key)[k] / qsum;
         }
@@ -1879,7 +1990,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
 
         // stage times non-decreasing in b and I (non-negative coefficients): the row
         // optimum is then monotone in the row, which the gamma-level pruning needs
-        const bool mono = s_par[1] >= 0.0 && s_par[2] >= 0.0 && s_par[3] >= 0.0 && s_par[4] >= 0.0 && C.dl >= 0.0;
+        mono = s_par[1] >= 0.0 && s_par[2] >= 0.0 && s_par[3] >= 0.0 && s_par[4] >= 0.0 && C.dl >= 0.0;
         // ---- per-gamma prologue, one gamma per thread:
         //  * the verify-work lower bound T_inf(gamma) >= sum_k vsl(I_k) + vc, in O(1): vsl is a
         //    quadratic in I, so the sum needs only sum I and sum I^2;
@@ -1895,12 +2006,14 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             const double Kd = (double)K;
             const bool one_fits = sm.jlo[K - 1] == 1;     // a batch of all K tasks fits the memory
             double one_min = dinf();
+            #pragma unroll 1
             for (int gi = tid; gi < ng; gi += kThreads) {
                 const int gamma = C.gmin + gi;
                 const double L = expected_tokens(s_par[0], gamma);
                 const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));
                 const DPConst D = make_dpconst(C, gamma, L, N, s_par[1], s_par[2], s_par[3], s_par[4]);
                 sm.dq[gi] = D;
+                if (PHASE == 1) sm.tinf[gi] = L;
                 sm.nq[gi] = N;
                 const double c = D.hv2 + D.g;
                 const double lbv = D.kv * (S2 + (D.g + c) * S1 + Kd * D.g * c) + D.kv * (1.0 + D.g) * D.Mx * (S1 + Kd * c) +
@@ -1928,6 +2041,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (warp == 0) {                 // queue: the gamma of the smallest bound first, then ascending
                 double v = dinf();
                 int a = ng;
+                #pragma unroll 1
                 for (int gi = lane; gi < ng; gi += 32)
                     if (sm.glb[gi] < v) { v = sm.glb[gi]; a = gi; }
                 for (int o = 16; o > 0; o >>= 1) {
@@ -1936,6 +2050,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     if (ov < v || (ov == v && oa < a)) { v = ov; a = oa; }
                 }
                 if (a >= ng) a = 0;                                  // all bounds NaN / inf
+                #pragma unroll 1
                 for (int pos = lane; pos < ng; pos += 32) sm.gord[pos] = pos == 0 ? a : (pos <= a ? pos - 1 : pos);
             }
             if (tid == 0) {
@@ -1945,6 +2060,102 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             }
             __syncthreads();
         }
+        for (int w = 0; w < kWarps; ++w) Tcom = uniform ? fmax(Tcom, sm.red[w]) : Tcom + sm.red[w];
+        if constexpr (PHASE == 1) {
+            // ---- prep record of scenario s (coalesced), and the outputs that do not need the DPs
+            const PrepView pv = prep_view(ws.prep + (size_t)s * C.prep_stride, K, ng);
+            #pragma unroll 1
+            for (int k = tid; k < K; k += kThreads) {
+                out.order[s * K + k] = sm.ord[k];
+                pv.Is[k] = sm.Is[k];
+                pv.jlo[k] = sm.jlo[k];
+            }
+            #pragma unroll 1
+            for (int k = tid; k < pfx_len(K); k += kThreads) { pv.pI[k] = sm.pI[k]; pv.pI2[k] = sm.pI2[k]; }
+            if (!bad && !bad_alpha) {
+                #pragma unroll 1
+                for (int gi = tid; gi < ng; gi += kThreads) {
+                    pv.glb[gi] = sm.glb[gi];
+                    pv.L[gi] = sm.tinf[gi];          // L, parked there by the prologue
+                    pv.N[gi] = sm.nq[gi];
+                }
+            }
+            if (tid == 0) {
+                pv.misc[0] = s_best;
+                pv.misc[1] = Tcom;
+                pv.flags[0] = (bad ? 1 : 0) | (bad_alpha ? 2 : 0) | (mono ? 4 : 0);
+                out.lat[3 * s + 1] = bad ? dnan() : Tcom;
+                if (bad || bad_alpha) {              // status 3 / 2: no DP runs (phase 2 skips it)
+                    out.lat[3 * s] = dnan();
+                    out.lat[3 * s + 2] = dnan();
+                    out.gamma[s] = -1;
+                    out.M[s] = 0;
+                    out.status[s] = bad ? 3 : 2;
+                }
+            }
+            if (bad || bad_alpha) {
+                #pragma unroll 1
+                for (int k = tid; k < K; k += kThreads) {
+                    out.bend[s * K + k] = 0;
+                    if (out.trace) out.trace[s * K + k] = 0;
+                    if (out.bgam) out.bgam[s * K + k] = 0;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+        } else {
+            // ---- PHASE 2: the prep record of scenario s -> shared memory
+            const PrepView pv = prep_view(ws.prep + (size_t)s * C.prep_stride, K, ng);
+            const int fl = pv.flags[0];
+            bad = fl & 1;
+            bad_alpha = (fl & 2) != 0;
+            mono = (fl & 4) != 0;
+            if (bad || bad_alpha) {              // every output written by phase 1
+                __syncthreads();
+                continue;
+            }
+            #pragma unroll 1
+            for (int k = tid; k < K; k += kThreads) {
+                sm.Is[k] = pv.Is[k];
+                sm.jlo[k] = pv.jlo[k];
+            }
+            #pragma unroll 1
+            for (int k = tid; k < pfx_len(K); k += kThreads) { sm.pI[k] = pv.pI[k]; sm.pI2[k] = pv.pI2[k]; }
+            const double c1d = in.coeffs ? in.coeffs[4 * s] : C.c1d, c2d = in.coeffs ? in.coeffs[4 * s + 1] : C.c2d;
+            const double c1v = in.coeffs ? in.coeffs[4 * s + 2] : C.c1v, c2v = in.coeffs ? in.coeffs[4 * s + 3] : C.c2v;
+            #pragma unroll 1
+            for (int gi = tid; gi < ng; gi += kThreads) {
+                sm.glb[gi] = pv.glb[gi];
+                const int N = pv.N[gi];
+                sm.nq[gi] = N;
+                sm.dq[gi] = make_dpconst(C, C.gmin + gi, pv.L[gi], N, c1d, c2d, c1v, c2v);
+            }
+            if (tid == 0) {
+                s_best = pv.misc[0];
+                Tcom = pv.misc[1];
+                sm.red[0] = Tcom;
+            }
+            __syncwarp();
+            Tcom = sm.red[0];
+            {   // queue: the gamma of the smallest bound first, then ascending
+                double v = dinf();
+                int a = ng;
+                #pragma unroll 1
+                for (int gi = lane; gi < ng; gi += 32)
+                    if (sm.glb[gi] < v) { v = sm.glb[gi]; a = gi; }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int oa = __shfl_xor_sync(0xffffffffu, a, o);
+                    if (ov < v || (ov == v && oa < a)) { v = ov; a = oa; }
+                }
+                if (a >= ng) a = 0;
+                #pragma unroll 1
+                for (int pos = lane; pos < ng; pos += 32) sm.gord[pos] = pos == 0 ? a : (pos <= a ? pos - 1 : pos);
+            }
+            __syncwarp();
+        }
+        if constexpr (PHASE != 1) {
         // ---- P3: each warp pulls gamma values and runs Algorithm 1
         const bool pbg = C.batch_policy == SDEDGE_BATCH_PER_BATCH_GAMMA;
         if (pbg) {
@@ -1964,9 +2175,27 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             // neither win nor tie -- it is dropped from the queue without a DP call
             const bool prune = SDEDGE_GAMMA_ABORT && mono && C.batch_policy == SDEDGE_BATCH_PROPOSED;
             const double mg = sizeof(R) == 8 ? 1e-11 : 1e-4;
+            // one warp and <= 32 gammas: lane p holds queue position p; the queue is a register mask
+            const bool lanes_q = kWarps == 1 && ng <= 32;
+            const int q_l = lanes_q && lane < ng ? sm.gord[lane] : 0;
+            const double glb_l = lanes_q && lane < ng ? sm.glb[q_l] : 0.0;
+            unsigned left = lanes_q ? (ng == 32 ? 0xffffffffu : ((1u << ng) - 1u)) : 0u;
             for (;;) {
-                // lane 0 takes the next G unpruned gammas of the queue (most promising first)
+                // the next G unpruned gammas of the queue (most promising first)
                 int mine = -1;
+                if (lanes_q) {
+                    const bool dead = prune && glb_l * (1.0 - mg) > s_best * (1.0 + mg);
+                    const unsigned deadm = __ballot_sync(0xffffffffu, ((left >> lane) & 1u) && dead);
+                    if ((deadm >> lane) & 1u) sm.tinf[q_l] = dinf();
+                    left &= ~deadm;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int pos = left ? __ffs(left) - 1 : -1;
+                        if (pos >= 0) left &= left - 1u;
+                        const int sel = __shfl_sync(0xffffffffu, q_l, pos >= 0 ? pos : 0);
+                        if (g == grp) mine = pos >= 0 ? sel : -1;
+                    }
+                } else {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     int sel = -1;
@@ -1982,6 +2211,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     sel = __shfl_sync(0xffffffffu, sel, 0);
                     if (g == grp) mine = sel;
                     if (g == 0 && sel < 0) break;
+                }
                 }
                 const int first = __shfl_sync(0xffffffffu, mine, 0);
                 if (first < 0) break;
@@ -2005,6 +2235,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     // 2, 3, ... in sorted order until the pipelined latency stops improving
                     short* jw = sm.jw + (size_t)warp * K;
                     auto plan = [&](int b) {
+                        #pragma unroll 1
                         for (int r = lane; r < K; r += 32) {
                             const int e = r + 1;
                             jw[r] = (short)((e % b == 0 || e == K) ? ((e - 1) / b) * b + 1 : 0);
@@ -2057,11 +2288,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             continue;
         }
 
-        double Tcom = 0.0, qsum = 0.0;       // eq:opt_w sums (per-warp partials in sm.red)
-        for (int w = 0; w < kWarps; ++w) {
-            Tcom = uniform ? fmax(Tcom, sm.red[w]) : Tcom + sm.red[w];
-            qsum += sm.red[kWarps + w];
-        }
+
         // ---- gamma* (smallest argmin, reading A7) and backtrack (reading A5)
         if (tid == 0) {
             int st = 0, gbest = -1, M = 0;
@@ -2074,6 +2301,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 gbest = best < dinf() ? 0 : -1;
                 if (gbest < 0) st = 1;
             } else {
+                #pragma unroll 1
                 for (int gi = 0; gi < ng; ++gi)
                     if (sm.tinf[gi] < best) { best = sm.tinf[gi]; gbest = gi; }
                 if (gbest < 0) st = 1;
@@ -2101,25 +2329,30 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         }
         __syncthreads();
         const int M = sm.ctl[2];
+        #pragma unroll 1
         for (int k = tid; k < K; k += kThreads) {
-            out.order[s * K + k] = sm.ord[k];
+            if (PHASE != 2) out.order[s * K + k] = sm.ord[k];
             out.bend[s * K + k] = k < M ? reinterpret_cast<const int*>(sm.key)[M - 1 - k] : 0;
         }
         if (out.bgam)                        // each batch's gamma (gamma* for all unless per-batch)
+            #pragma unroll 1
             for (int k = tid; k < K; k += kThreads)
                 out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + reinterpret_cast<const int*>(sm.key)[M - 1 - k] - 1]
                                                        : C.gmin + sm.ctl[4];
         if (out.trace) {                     // S vector of gamma* (row choices; 0 unless status 0)
             const short* S = Scta + (size_t)max(sm.ctl[4], 0) * K;
+            #pragma unroll 1
             for (int k = tid; k < K; k += kThreads) out.trace[s * K + k] = M > 0 ? (int32_t)S[k] : 0;
         }
 
         __syncthreads();
+        }   // PHASE != 1
     }
     if (out.work) {
         __syncthreads();
         if (tid < 5) {
             unsigned long long v = 0;
+            #pragma unroll 1
             for (int t = 0; t < kThreads; ++t) v += s_work[t * 5 + tid];
             atomicAdd(out.work + tid, v);
         }
@@ -2587,16 +2820,38 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     // row state in shared memory when it keeps >= 3 CTAs (12 warps) per SM
     // row state in shared memory when it keeps >= 3 CTAs per SM (untiled), always for TILE == 2
     C.rows_in_smem = TILE == 2 ? 1 : (!TILE && smem_bytes<R, G>(C.K, C.ng, 1, 0) <= (size_t)(220 * 1024 / 3) ? 1 : 0);
-    const size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE == 1, TILE == 2 ? rs_pad(C.K, 32 / G) : 0);
+    size_t sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE == 1, TILE == 2 ? rs_pad(C.K, 32 / G) : 0);
+    // Envelope-segment pool of the first pass in shared memory (TILE == 2) when the draft stage is
+    // the slower one: then envelopes have several segments and the merge / sums walk the pool on
+    // every update.  The decision compares the per-token cost of a draft pass with a verify pass
+    // (the params' coefficients; per-scenario coefficients do not change it -- it only places
+    // memory).  A DP that outgrows this smaller pool is redone by the worst-case pass.
+    const double draft_per_tok = C.c1d * C.Jd * (double)C.hd, verify_per_tok = C.c1v * C.Jv * (double)C.hv;
+    C.pool_smem = (SDEDGE_POOL_SMEM && TILE == 2 && G == 1 && kWarps == 1 && !(flags & SDEDGE_FLAG_TINY_POOL) && draft_per_tok > verify_per_tok) ? 1 : 0;
+    C.pool_cap_smem = ((2LL * (C.K + 1) + 32) + 7) & ~7LL;
+    if (C.pool_smem) sb += (pool_bytes<R>(C.pool_cap_smem) + 15) & ~(size_t)15;
     if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     C.rows_stride = (long long)((rb + 255) & ~(size_t)255);
 
-    // (the tiled DP keeps its rows in global memory: no RSMEM instantiation for it)
-    auto k_main = (TILE != 1 && C.rows_in_smem) ? solve_kernel<R, ALGO, TILE == 1 ? 0 : 1, G, TILE>
-                                                : solve_kernel<R, ALGO, 0, G, TILE>;
-    auto k_big = k_main;
+    // tiled (TILE != 0): two kernels, prep (PHASE 1) then the DPs (PHASE 2); otherwise one fused kernel
+    using KFn = void (*)(const Consts, const Inputs, const Outputs, long long, Work, int);
+    KFn k_main;
+    if constexpr (TILE == 2) k_main = solve_kernel<R, ALGO, 1, G, 2, 2>;
+    else if constexpr (TILE == 1) k_main = solve_kernel<R, ALGO, 0, G, 1, 2>;
+    else k_main = C.rows_in_smem ? solve_kernel<R, ALGO, 1, G, 0, 0> : solve_kernel<R, ALGO, 0, G, 0, 0>;
+    KFn k_big = k_main;
+    // the prep kernel does not depend on the row store: one instantiation serves TILE 1 and 2
+    KFn k_prep = TILE ? solve_kernel<R, ALGO, 0, G, 1, 1> : k_main;
+    const size_t sb_prep = smem_bytes<R, G>(C.K, C.ng, 0, 0);
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    int occ_prep = 0;
+    if (TILE) {
+        CU(cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb_prep));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_prep, k_prep, kThreads, sb_prep));
+        if (occ_prep < 1) return fail(-1, "prep kernel does not fit on an SM");
+    }
+    C.prep_stride = TILE ? (long long)prep_stride(C.K, C.ng) : 0;
     int occ = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_main, kThreads, sb));
     if (occ < 1) return fail(-1, "kernel does not fit on an SM");
@@ -2619,7 +2874,8 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
 
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
-    const size_t o_next = take(2 * sizeof(unsigned long long) + sizeof(unsigned int));
+    const size_t o_next = take(3 * sizeof(unsigned long long) + sizeof(unsigned int));
+    const size_t o_prep = take((size_t)n * C.prep_stride);
     const size_t o_S = take((size_t)std::max(grid, grid_big) * (C.ng + 1) * C.K * sizeof(short));
     const size_t o_list = take((size_t)n * sizeof(long long));
     const size_t o_rows = take(C.rows_in_smem ? 0 : (size_t)std::max(slots, slots_big) * C.rows_stride);
@@ -2628,12 +2884,13 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     const size_t o_ybuf = take((size_t)grid * C.ybuf_stride * sizeof(double));
     unsigned char* wsb = nullptr;
     if (int rc = ws_alloc(reinterpret_cast<void**>(&wsb), off, st)) return rc;
-    CU(cudaMemsetAsync(wsb + o_next, 0, 2 * sizeof(unsigned long long) + sizeof(unsigned int), st));
+    CU(cudaMemsetAsync(wsb + o_next, 0, 3 * sizeof(unsigned long long) + sizeof(unsigned int), st));
 
     Work w;
     w.S = reinterpret_cast<short*>(wsb + o_S);
     w.next = reinterpret_cast<unsigned long long*>(wsb + o_next);
-    w.ovf_count = reinterpret_cast<unsigned int*>(wsb + o_next + 2 * sizeof(unsigned long long));
+    w.ovf_count = reinterpret_cast<unsigned int*>(wsb + o_next + 3 * sizeof(unsigned long long));
+    w.prep = wsb + o_prep;
     w.ovf_list = reinterpret_cast<long long*>(wsb + o_list);
     w.rows = wsb + o_rows;
     w.ybuf = reinterpret_cast<double*>(wsb + o_ybuf);
@@ -2642,12 +2899,24 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (n > 0) {
         C.pool_cap = cap_main;
         w.pool = wsb + o_pool;
+        if (TILE) {
+            const long long grid_prep = std::min((long long)nsm * occ_prep, n);
+            const int tq = kt_begin(KT_PREP, st);
+            k_prep<<<(unsigned)grid_prep, kThreads, sb_prep, st>>>(C, in, out, n, w, 0);
+            kt_end(tq, st);
+            ++launches;
+            CU(cudaGetLastError());
+        }
+        int tq = kt_begin(KT_MAIN, st);
         k_main<<<(unsigned)grid, kThreads, sb, st>>>(C, in, out, n, w, 0);
+        kt_end(tq, st);
         ++launches;
         CU(cudaGetLastError());
         C.pool_cap = cap_big;
         w.pool = wsb + o_pool_big;
+        tq = kt_begin(KT_BIG, st);
         k_big<<<(unsigned)grid_big, kThreads, sb, st>>>(C, in, out, n, w, 1);
+        kt_end(tq, st);
         ++launches;
         CU(cudaGetLastError());
     }
@@ -2994,6 +3263,29 @@ int sdedge_ipc_close(void* dev_ptr, uint64_t offset)
     g_err[0] = 0;
     if (!dev_ptr) return fail(-1, "null argument");
     CU(cudaIpcCloseMemHandle(static_cast<unsigned char*>(dev_ptr) - offset));
+    return 0;
+}
+
+int sdedge_kernel_timing(int32_t enable)
+{
+    g_err[0] = 0;
+    g_kt.on = enable != 0;
+    g_kt.used = 0;
+    return 0;
+}
+
+int sdedge_kernel_times(double* ms, int32_t* launches)
+{
+    g_err[0] = 0;
+    if (!ms) return fail(-1, "null argument");
+    for (int k = 0; k < 4; ++k) { ms[k] = 0.0; if (launches) launches[k] = 0; }
+    for (int q = 0; q < g_kt.used; ++q) {
+        CU(cudaEventSynchronize(g_kt.ev[q][1]));
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, g_kt.ev[q][0], g_kt.ev[q][1]));
+        ms[g_kt.kind[q]] += t;
+        if (launches) ++launches[g_kt.kind[q]];
+    }
     return 0;
 }
 
