@@ -108,6 +108,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--batching-policy", type=int, default=0,
+                    help="0 proposed (Algorithm 1), 1 SD w/o pipeline, 2-5 paper baselines, 6 per-batch gamma")
     return ap.parse_args()
 
 
@@ -213,6 +215,7 @@ def run_reference(args):
     if rank != 0:
         return
     pd, _, n_total = scengen.config(args.config, 0, 1, pair=args.pair)
+    pd = dict(pd, batching_policy=args.batching_policy)
     cores = os.cpu_count() or 1
     per_step = args.cpu_sample or cores
     rates, times = [], []
@@ -225,7 +228,7 @@ def run_reference(args):
     value = per_step * len(times) / sum(times)
     cfg = config_of(args, n_total, ws)
     cfg.update(K=pd["K"], gamma=[pd["gamma_min"], pd["gamma_max"]],
-               pair=f"{scengen_pair(pd)}")
+               pair=f"{scengen_pair(pd)}", batching_policy=args.batching_policy)
     line = {"impl": "reference", "metric": "scenarios solved/sec (fp64)", "value": value,
             "unit": "scenarios/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "strong",
@@ -272,6 +275,7 @@ def main():
     sd.lib()
 
     pd, _, n_cfg = scengen.config(args.config, 0, 1, pair=args.pair)
+    pd = dict(pd, batching_policy=args.batching_policy)
     strong = args.scaling == "strong"
     if strong:
         n_total = args.n or n_cfg
@@ -423,6 +427,7 @@ def main():
                        "sample": f"failed: {e}"}
         cfg = config_of(args, n, ws)
         cfg.update(K=K, gamma=[pd["gamma_min"], pd["gamma_max"]], pair=scengen_pair(pd),
+                   batching_policy=args.batching_policy,
                    scenarios_per_gpu=n, total_scenarios=n_total,
                    parallelism=(f"scenario-shard x{ws}" + (", outputs gathered to cuda:0 by the solve's own "
                                                           "NVLink peer stores (CUDA IPC)" if ws > 1 and strong

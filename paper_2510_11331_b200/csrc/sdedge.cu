@@ -88,7 +88,7 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #define SDEDGE_TILE_SHFL_ARGMIN 1
 #endif
 #ifndef SDEDGE_POOL_SMEM
-#define SDEDGE_POOL_SMEM 1    // allow the first-pass envelope pool in shared memory (draft-bound pairs)
+#define SDEDGE_POOL_SMEM 0    // 1: first-pass envelope pool in shared memory for draft-bound pairs (measured slower: 4.12 vs 4.33 M/s, r2k)
 #endif
 #ifndef SDEDGE_RS_MAX_K
 #define SDEDGE_RS_MAX_K 160   // tiled DP keeps its row store in shared memory up to this K
@@ -531,9 +531,70 @@ __device__ inline void warp_bitonic(unsigned long long (&x)[E], int lane)
     }
 }
 
+// 32-bit keys (I << 7 | e, valid when 0 <= I < 2^24 and K <= 128): half the shuffles and compares
+template <int E>
+__device__ inline void warp_bitonic32(unsigned (&x)[E], int lane)
+{
+    constexpr int P = 32 * E;
+#pragma unroll 1
+    for (int sz = 2; sz <= P; sz <<= 1) {
+#pragma unroll 1
+        for (int st = sz >> 1; st > 0; st >>= 1) {
+            if (st >= E) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int e = lane * E + r;
+                    const unsigned o = __shfl_xor_sync(0xffffffffu, x[r], st / E);
+                    const bool keep_min = ((e & sz) == 0) == ((e & st) == 0);
+                    x[r] = keep_min ? min(o, x[r]) : max(o, x[r]);
+                }
+            } else {
+#pragma unroll
+                for (int sv = 1; sv < E; sv <<= 1) {
+                    if (st != sv) continue;
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        if (r & sv) continue;
+                        const unsigned a = x[r], b = x[r | sv];
+                        if ((a > b) == (((lane * E + r) & sz) == 0)) { x[r] = b; x[r | sv] = a; }
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int E>
 __device__ inline void warp_sort_tasks(const int* I, int* ord, int* Is, int K, int lane)
 {
+    static_assert(32 * E <= 128, "the 32-bit keys hold a 7-bit index");
+    int mn = 0x7fffffff, mx = -0x7fffffff - 1;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int e = lane * E + r;
+        if (e < K) { mn = min(mn, I[e]); mx = max(mx, I[e]); }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (mn >= 0 && mx < (1 << 24)) {
+        unsigned y[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int e = lane * E + r;
+            y[r] = e < K ? ((unsigned)I[e] << 7) | (unsigned)e : 0xffffffffu;
+        }
+        warp_bitonic32<E>(y, lane);
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int e = lane * E + r;
+            if (e < K) {
+                const int k = (int)(y[r] & 127u);
+                ord[e] = k;
+                Is[e] = I[k];
+            }
+        }
+        return;
+    }
     unsigned long long x[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
@@ -1410,7 +1471,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                                  RowRec<R>* stage, unsigned long long* bars, unsigned& bar_phase,
                                  unsigned st0, unsigned tstride, const unsigned char* rw0, long long rwstride,
                                  int gi, short* S, bool* overflow, WorkCount& wc, long long* top_s, bool active,
-                                 const double* best_s, double lbv)
+                                 const double* best_s, double lbv, bool mono)
 {
     constexpr int GL = 32 / G;
     const int lane = threadIdx.x & 31;
@@ -1532,6 +1593,20 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             // this lane's candidates in the chunk: predecessors max(a, pst) .. e-1
             const int lo = max(pst - a, 0), hi = e - a;
             n_cand += (unsigned)max(hi - lo, 0);
+#if SDEDGE_PRUNE
+            // whole-chunk skip: with coefficients >= 0 the row values Upsilon[p,0,0] = key
+            // are non-decreasing in p (5.2d), so every predecessor of the chunk has key >= key[a] and
+            // batch size >= i - (e-1): LB1 >= key[a] + (i-e+1) vsl + vc.  A chunk whose bound exceeds
+            // every lane's threshold (key[a] shaded by 1e-13, fp32 1e-6, against rounding) is skipped
+            if (mono) {
+                const R ka = buf[0].key * (sizeof(R) == 8 ? (R)(1.0 - 1e-13) : (R)(1.0 - 1e-6));
+                const R lbc = ka + (R)fma(bda - (double)(e - a - 1), rc.vsl, rc.vc);
+                if (__all_sync(0xffffffffu, !own || lbc > thr)) {
+                    if (!RS) __syncwarp();
+                    continue;
+                }
+            }
+#endif
             // pass 1 (independent, unrolled): the bound of every predecessor of the
             // chunk against the threshold at the chunk's start -- a superset of the
             // survivors, since the threshold only falls
@@ -1839,6 +1914,56 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         const int32_t* Ig = in.I + s * K;
         const double* pg = in.p + s * K;
         const double* gg = in.g + s * K;
+        // t*_com and w* sums (eq:opt_w); s1, s2 = sum I_k, sum I_k^2 (exact integers)
+        double tc = 0.0, q = 0.0, s1 = 0.0, s2 = 0.0;
+        // fast path: one warp, K <= 128, K % 4 == 0, 16-byte aligned rows -- every lane takes 4
+        // consecutive tasks with one int4 and four double2 loads, validates them and computes their
+        // bandwidth terms in registers, and writes w* straight from registers after the reductions
+        const bool fast = kWarps == 1 && K <= 128 && (K & 3) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(Ig) | reinterpret_cast<uintptr_t>(pg) |
+                            reinterpret_cast<uintptr_t>(gg)) & 15u) == 0;
+        if (fast) {
+            const int k0 = 4 * lane;
+            double u[4] = {0.0, 0.0, 0.0, 0.0};
+            if (k0 < K) {
+                const int4 Iv = reinterpret_cast<const int4*>(Ig)[lane];
+                const double2 pa = reinterpret_cast<const double2*>(pg)[2 * lane];
+                const double2 pb = reinterpret_cast<const double2*>(pg)[2 * lane + 1];
+                const double2 ga = reinterpret_cast<const double2*>(gg)[2 * lane];
+                const double2 gb = reinterpret_cast<const double2*>(gg)[2 * lane + 1];
+                const int Ik[4] = {Iv.x, Iv.y, Iv.z, Iv.w};
+                const double pk[4] = {pa.x, pa.y, pb.x, pb.y}, gk[4] = {ga.x, ga.y, gb.x, gb.y};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    sm.I[k0 + r] = Ik[r];
+                    if (Ik[r] < 1 || !(pk[r] > 0.0) || !(gk[r] > 0.0) || !isfinite(pk[r]) || !isfinite(gk[r])) bad = 1;
+                    const double Ikd = (double)Ik[r];
+                    s1 += Ikd;
+                    s2 += Ikd * Ikd;
+                    const double sk = log2(1.0 + pk[r] * gk[r] / C.sigma2);
+                    if (uniform) {
+                        tc = fmax(tc, C.lambda * Ikd / ((1.0 / K) * C.Bw * sk));
+                    } else {
+                        tc += C.lambda * Ikd / (C.Bw * sk);
+                        u[r] = Ikd / sk;
+                        q += u[r];
+                    }
+                }
+            }
+            bad = __any_sync(0xffffffffu, bad);
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ot = __shfl_xor_sync(0xffffffffu, tc, o);
+                tc = uniform ? (ot > tc ? ot : tc) : tc + ot;
+                q += __shfl_xor_sync(0xffffffffu, q, o);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (out.w && k0 < K)
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    out.w[s * K + k0 + r] = bad ? dnan() : uniform ? 1.0 / K : u[r] / q;
+            __syncwarp();
+        } else {
         #pragma unroll 1
         for (int k = tid; k < K; k += kThreads) {
             const int Ik = Ig[k];
@@ -1847,6 +1972,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (Ik < 1 || !(pk > 0.0) || !(gk > 0.0) || !isfinite(pk) || !isfinite(gk)) bad = 1;
         }
         bad = __syncthreads_or(bad);
+        }
         // ---- stable ascending sort by I_k (reading A13): bitonic sort of the unique keys
         // (I_k biased to unsigned) << 32 | k, padded to a power of two with ~0 -- O(K log^2 K / threads)
         if (kWarps == 1 && K <= 128) {       // in registers: one warp, 4 keys per lane
@@ -1919,8 +2045,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         }
         // ---- t*_com and w* (eq:opt_w; reading A14: p_k g_k / sigma^2), or the
         // uniform baseline w_k = 1/K with T_com = max_k T_k,com (eq:ul_latency)
-        double tc = 0.0, q = 0.0, s1 = 0.0, s2 = 0.0;   // s1, s2: sum I_k, sum I_k^2 (exact integers)
-        if (!bad)
+        if (!bad && !fast)
             #pragma unroll 1
             for (int k = tid; k < K; k += kThreads) {
                 const double Ikd = (double)sm.I[k];
@@ -1937,6 +2062,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     reinterpret_cast<double*>(sm.key)[k] = u;   // w*_k = u_k / sum u (the sort keys are dead)
                 }
             }
+        if (!fast)
         for (int o = 16; o > 0; o >>= 1) {
             const double ot = __shfl_xor_sync(0xffffffffu, tc, o);
             tc = uniform ? fmax(tc, ot) : tc + ot;
@@ -1972,7 +2098,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         }
         __syncthreads();
         bad_alpha = !(s_par[0] > 0.0 && s_par[0] < 1.0);
-        if (out.w) {                         // w* (eq:opt_w): known before any DP runs
+        if (out.w && !fast) {                // w* (eq:opt_w): known before any DP runs
             double qsum = 0.0;
             for (int w = 0; w < kWarps; ++w) qsum += sm.red[kWarps + w];
             #pragma unroll 1
@@ -2229,7 +2355,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     t = dp_gamma_tiled<R, G, TILE == 2>(C, sm, rw, pl, tb, stage, bars, bar_phase, st0, tb_stride, rw0,
                                              C.rows_stride, gi,
                                              Sg, &ovf, wc, &s_top[warp * G + grp], active,
-                                             (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr, sm.glb[gi]);
+                                             (SDEDGE_GAMMA_ABORT && mono) ? &s_best : nullptr, sm.glb[gi], mono);
                 } else if (kBase && C.batch_policy == SDEDGE_BATCH_HEURISTIC) {
                     // heuristic batching (reading B5): equal batches of size
                     // 2, 3, ... in sorted order until the pipelined latency stops improving
