@@ -95,7 +95,7 @@ def dense_work(pd, sc):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--algo", choices=["envelope", "dense"], default="envelope")
@@ -108,6 +108,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--gather", choices=["chunked", "fused"], default="chunked",
+                    help="multi-GPU gather: chunked solves + copy-engine peer copies overlapped with the next "
+                         "chunk's solve, or the kernels' own peer stores")
+    ap.add_argument("--gather-chunks", type=int, default=6)
     ap.add_argument("--batching-policy", type=int, default=0,
                     help="0 proposed (Algorithm 1), 1 SD w/o pipeline, 2-5 paper baselines, 6 per-batch gamma")
     return ap.parse_args()
@@ -144,10 +148,11 @@ class ClockSampler:
 
     def __init__(self, uuid):
         self.uuid, self.rows, self.proc = uuid, [], None
+        self.t0 = self.t1 = None             # the timed region (host clock), set by mark()
 
     def __enter__(self):
         try:
-            cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50"]
+            cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20"]
             if self.uuid:
                 cmd += ["-i", self.uuid]
             self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -161,7 +166,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append([time.time()] + parts)
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -171,15 +176,23 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        # samples taken inside the timed region (the sampler runs from before the warm-up)
+        rows = [r[1:] for r in self.rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[q] for r in self.rows for q in range(4) if r[3 + q] == "Active"})
+        reasons = sorted({names[q] for r in rows for q in range(4) if r[3 + q] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "window_s": (self.t1 or 0) - (self.t0 or 0)}
 
 
 def cpu_model():
@@ -316,9 +329,39 @@ def main():
             gout = lay.rows(peer[0], s0)
         dist.barrier()
 
+    def solve_into(out, count, c0=0, c1=None):
+        c1 = n if c1 is None else c1
+        sl = (lambda t: t) if (c0 == 0 and c1 == n) else (lambda t: t[c0:c1])
+        sd.solve(pd, sl(d["I"]), sl(d["p"]), sl(d["g"]), sl(d["alpha"]), None, out=out, stream=stream,
+                 precision=prec, algo=algo, work_counters=work if count else None)
+
+    # chunked gather (ranks >= 1): solve chunk c into rank-local arrays, then the copy engines move
+    # it into cuda:0's arrays over NVLink while chunk c+1 is solved; the step ends when the copies do
+    chunked = ws > 1 and strong and rank > 0 and args.gather == "chunked"
+    if chunked:
+        lay_loc = GatherLayout(n, K, True)
+        lbuf = torch.empty(lay_loc.nbytes, dtype=torch.uint8, device=dev)
+        lviews = lay_loc.views(torch, lbuf)
+        copy_stream = torch.cuda.Stream(dev)
+        nch = max(1, min(args.gather_chunks, n))
+        # decreasing chunk sizes (weights nch, nch-1, .., 1): only the last, smallest chunk's copy is exposed
+        wsum = nch * (nch + 1) // 2
+        cum = [n * sum(range(nch, nch - c, -1)) // wsum for c in range(nch + 1)]
+        bounds = [(cum[c], cum[c + 1]) for c in range(nch) if cum[c + 1] > cum[c]]
+        nch = len(bounds)
+        evs = [torch.cuda.Event() for _ in range(nch)]
+
     def step(out, count=False):
-        sd.solve(pd, d["I"], d["p"], d["g"], d["alpha"], None, out=out, stream=stream, precision=prec,
-                 algo=algo, work_counters=work if count else None)
+        if not chunked or out is local_out:
+            solve_into(out, count)
+            return
+        for c, (c0, c1) in enumerate(bounds):
+            solve_into({k: (v[c0:c1] if v is not None else None) for k, v in lviews.items()}, count, c0, c1)
+            evs[c].record(stream)
+            copy_stream.wait_event(evs[c])
+            for dst, src, nb in lay.chunk_copies(peer[0], s0, lay_loc, lbuf.data_ptr(), c0, c1):
+                sd.copy_async(dst, src, nb, copy_stream)
+        stream.wait_stream(copy_stream)
 
     def timed(out, count, clk=None):
         if ws > 1:
@@ -334,21 +377,25 @@ def main():
             dist.barrier()
         return e0.elapsed_time(e1) * 1e-3
 
-    for _ in range(args.warmup):
-        step(gout)
-    torch.cuda.synchronize()
-    launches_per_step = sd.sdedge_last_launch_count()
-
     uuid = None
     try:
         uuid = str(torch.cuda.get_device_properties(dev).uuid)
         uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
     except Exception:
         pass
+    clk = ClockSampler(uuid).__enter__()    # from before the warm-up: samples cover the whole timed region
+    for _ in range(args.warmup):
+        step(gout)
+    torch.cuda.synchronize()
+    launches_per_step = sd.sdedge_last_launch_count()
+    time.sleep(0.3)                          # the sampler is running by now
     work.zero_()
     sd.sdedge_kernel_timing(True)            # per-kernel CUDA events on the solve's stream
-    with ClockSampler(uuid) as clk:
-        el = timed(gout, True)
+    clk.mark(True)
+    el = timed(gout, True)
+    clk.mark(False)
+    time.sleep(0.05)
+    clk.__exit__(None, None, None)
     ktimes = sd.sdedge_kernel_times()
     sd.sdedge_kernel_timing(False)
     el_max = max_over_ranks(el, dist, dev)
@@ -426,12 +473,15 @@ def main():
                 cpu = {"value": None, "unit": "scenarios/s", "cores": cores, "kind": "oracle",
                        "sample": f"failed: {e}"}
         cfg = config_of(args, n, ws)
+        gdesc = ("the solves' own NVLink peer stores into cuda:0's arrays (CUDA IPC)" if args.gather == "fused" else
+                 f"{args.gather_chunks} chunked solves of decreasing size per rank, each chunk copied into cuda:0's "
+                 f"arrays by the copy engines over NVLink (CUDA IPC) while the next is solved; rank 0 solves "
+                 f"into them directly")
         cfg.update(K=K, gamma=[pd["gamma_min"], pd["gamma_max"]], pair=scengen_pair(pd),
                    batching_policy=args.batching_policy,
                    scenarios_per_gpu=n, total_scenarios=n_total,
-                   parallelism=(f"scenario-shard x{ws}" + (", outputs gathered to cuda:0 by the solve's own "
-                                                          "NVLink peer stores (CUDA IPC)" if ws > 1 and strong
-                                                          else "")))
+                   parallelism=(f"scenario-shard x{ws}" + (f", outputs gathered to cuda:0 inside the timed step: {gdesc}"
+                                                          if ws > 1 and strong else "")))
         line = {
             "metric": "scenarios solved/sec (fp64)" if prec == 0 else "scenarios solved/sec (fp32 variant)",
             "value": n_total / (el_max / args.steps),

@@ -220,6 +220,9 @@ int sdedge_brute_force(const sdedge_scenarios* scenarios, int64_t n, const sdedg
 int sdedge_ipc_export(const void* dev_ptr, void* handle, uint64_t* offset);
 int sdedge_ipc_open(const void* handle, uint64_t offset, void** dev_ptr);
 int sdedge_ipc_close(void* dev_ptr, uint64_t offset);
+/* Asynchronous device-to-device copy on `stream` (a cudaStream_t), e.g. a finished chunk of a rank's
+ * outputs into cuda:0's peer-mapped arrays by the copy engines while the next chunk is solved. */
+int sdedge_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 
 /* Per-kernel timing for measurement (bench.py's roofline): sdedge_kernel_timing(1) clears the
  * record and starts bracketing every launch the solve calls on this thread enqueue with CUDA

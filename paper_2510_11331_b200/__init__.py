@@ -23,7 +23,7 @@ FLAG_TINY_POOL, FLAG_HEURISTIC_HALF = 1, 2
 EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
                     "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
                     "sdedge_abi_version", "sdedge_pipe_peak", "sdedge_ipc_export", "sdedge_ipc_open",
-                    "sdedge_ipc_close", "sdedge_kernel_timing", "sdedge_kernel_times")
+                    "sdedge_ipc_close", "sdedge_kernel_timing", "sdedge_kernel_times", "sdedge_copy_async")
 
 
 class SdedgeModel(C.Structure):
@@ -82,6 +82,8 @@ def lib() -> C.CDLL:
         L.sdedge_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
         L.sdedge_ipc_open.restype = C.c_int
         L.sdedge_ipc_open.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.sdedge_copy_async.restype = C.c_int
+        L.sdedge_copy_async.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
         L.sdedge_ipc_close.restype = C.c_int
         L.sdedge_ipc_close.argtypes = [C.c_void_p, C.c_uint64]
         L.sdedge_kernel_timing.restype = C.c_int
@@ -282,6 +284,14 @@ def ipc_open(handle: bytes, offset: int) -> int:
     if rc != 0:
         raise RuntimeError(f"sdedge_ipc_open failed ({rc}): {sdedge_last_error()}")
     return p.value
+
+
+def copy_async(dst: int, src: int, nbytes: int, stream) -> None:
+    """Device-to-device copy on `stream` (torch stream or raw handle); peer pointers allowed."""
+    st = stream if isinstance(stream, int) else int(stream.cuda_stream)
+    rc = lib().sdedge_copy_async(dst, src, nbytes, st)
+    if rc != 0:
+        raise RuntimeError(f"sdedge_copy_async failed ({rc}): {sdedge_last_error()}")
 
 
 def ipc_close(ptr: int, offset: int) -> None:

@@ -624,7 +624,9 @@ struct Smem {
     double* pI;    // [K/kPfx + 2] prefix sums of the sorted I (exact integers) at rows 0, kPfx, 2 kPfx, ..
     double* pI2;   // [K/kPfx + 2] ... of the sorted I^2 (the last entry: the total)
     int* nq;       // [ng] N_gamma (per-batch-gamma policy)
-    DPConst* dq;   // [ng] stage-time constants per gamma (per-batch-gamma policy)
+    DPConst* dq;   // [ng] stage-time constants per gamma
+    unsigned char* rec;          // DP kernel: two prep-record buffers (current, prefetched next)
+    unsigned long long* rbar;    // their mbarriers
     short* jlo;    // [K] first feasible j of row i (memory window), > i if none
     short* jf;     // [K] fixed-plan policies: start j of the batch ending at row i, 0 if none
     short* jw;     // [kWarps][K] heuristic batching: the plan under evaluation
@@ -666,52 +668,88 @@ __host__ __device__ inline int sort_len(int K)
     return p;
 }
 
-template <typename R, int G>
-__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile, int row_pad = 0)
+// Shared-memory layout of one CTA (carve when s != nullptr, else just size it).  rec > 0 is the DP
+// kernel of the two-kernel path: it keeps two prep-record buffers of rec bytes (the current
+// scenario's and the prefetched next one's, filled by TMA bulk copies) and points Is, jlo, pI, pI2
+// and glb into them, so it has no arrays of its own for those (nor for I, ord and the sort keys).
+__host__ __device__ inline size_t smem_layout(unsigned char* base, int K, int ng, int rec, Smem* s)
 {
     size_t b = 0;
-    b += 3 * (size_t)K * sizeof(int);
-    b = (b + 15) & ~(size_t)15;
-    b += (size_t)sort_len(K) * sizeof(unsigned long long);
-    b += (size_t)ng * (sizeof(double) + 2 * sizeof(int));
-    b = (b + 15) & ~(size_t)15;
-    b += (size_t)ng * sizeof(DPConst);
-    b += 2 * (size_t)pfx_len(K) * sizeof(double);
-    b += (size_t)(2 + kWarps) * K * sizeof(short);
-    b = (b + 15) & ~(size_t)15;
-    b += (size_t)ng * sizeof(double) + 5 * kWarps * sizeof(double) + 8 * sizeof(int) + sizeof(long long) * 2;
-    b = (b + 15) & ~(size_t)15;
+    auto at = [&](size_t bytes, size_t align) -> unsigned char* {
+        b = (b + align - 1) & ~(align - 1);
+        unsigned char* p = base ? base + b : nullptr;
+        b += bytes;
+        return p;
+    };
+    if (rec > 0) {
+        unsigned char* r0 = at((size_t)2 * rec, 16);
+        unsigned char* bars = at(2 * sizeof(unsigned long long), 8);
+        if (s) {
+            s->rec = r0;
+            s->rbar = reinterpret_cast<unsigned long long*>(bars);
+            s->I = s->Is = s->ord = nullptr;
+            s->key = nullptr;
+        }
+    } else {
+        unsigned char* pI_ = at((size_t)K * sizeof(int), 16);
+        unsigned char* pIs = at((size_t)K * sizeof(int), 4);
+        unsigned char* pord = at((size_t)K * sizeof(int), 4);
+        unsigned char* pkey = at((size_t)sort_len(K) * sizeof(unsigned long long), 16);
+        if (s) {
+            s->I = reinterpret_cast<int*>(pI_);
+            s->Is = reinterpret_cast<int*>(pIs);
+            s->ord = reinterpret_cast<int*>(pord);
+            s->key = reinterpret_cast<unsigned long long*>(pkey);
+            s->rec = nullptr;
+            s->rbar = nullptr;
+        }
+    }
+    unsigned char* pglb = rec > 0 ? nullptr : at((size_t)ng * sizeof(double), 8);
+    unsigned char* pgord = at((size_t)ng * sizeof(int), 4);
+    unsigned char* pnq = at((size_t)ng * sizeof(int), 4);
+    unsigned char* pdq = at((size_t)ng * sizeof(DPConst), 16);
+    unsigned char* ppI = rec > 0 ? nullptr : at((size_t)pfx_len(K) * sizeof(double), 8);
+    unsigned char* ppI2 = rec > 0 ? nullptr : at((size_t)pfx_len(K) * sizeof(double), 8);
+    unsigned char* pjlo = rec > 0 ? nullptr : at((size_t)K * sizeof(short), 2);
+    unsigned char* pjf = at((size_t)K * sizeof(short), 2);
+    unsigned char* pjw = at((size_t)kWarps * K * sizeof(short), 2);
+    unsigned char* ptinf = at((size_t)ng * sizeof(double), 16);
+    unsigned char* pred = at(5 * kWarps * sizeof(double), 8);
+    unsigned char* psid = at(2 * sizeof(long long), 8);
+    unsigned char* pctl = at(8 * sizeof(int), 4);
+    unsigned char* prows = at(0, 16);
+    if (s) {
+        s->glb = reinterpret_cast<double*>(pglb);
+        s->gord = reinterpret_cast<int*>(pgord);
+        s->nq = reinterpret_cast<int*>(pnq);
+        s->dq = reinterpret_cast<DPConst*>(pdq);
+        s->pI = reinterpret_cast<double*>(ppI);
+        s->pI2 = reinterpret_cast<double*>(ppI2);
+        s->jlo = reinterpret_cast<short*>(pjlo);
+        s->jf = reinterpret_cast<short*>(pjf);
+        s->jw = reinterpret_cast<short*>(pjw);
+        s->tinf = reinterpret_cast<double*>(ptinf);
+        s->red = reinterpret_cast<double*>(pred);
+        s->sid = reinterpret_cast<long long*>(psid);
+        s->ctl = reinterpret_cast<int*>(pctl);
+        s->rows = prows;
+    }
+    return (b + 15) & ~(size_t)15;
+}
+
+template <typename R, int G>
+__host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile, int row_pad = 0, int rec = 0)
+{
+    size_t b = smem_layout(nullptr, K, ng, rec, nullptr);
     if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K + row_pad);
     if (tile) b += (size_t)kWarps * G * tile_bytes<R, G>();
     return b;
 }
 
-__device__ inline Smem carve_smem(unsigned char* base, int K, int ng)
+__device__ inline Smem carve_smem(unsigned char* base, int K, int ng, int rec = 0)
 {
     Smem s;
-    size_t b = 0;
-    s.I = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
-    s.Is = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
-    s.ord = reinterpret_cast<int*>(base + b); b += (size_t)K * sizeof(int);
-    b = (b + 15) & ~(size_t)15;
-    s.key = reinterpret_cast<unsigned long long*>(base + b); b += (size_t)sort_len(K) * sizeof(unsigned long long);
-    s.glb = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
-    s.gord = reinterpret_cast<int*>(base + b); b += (size_t)ng * sizeof(int);
-    s.nq = reinterpret_cast<int*>(base + b); b += (size_t)ng * sizeof(int);
-    b = (b + 15) & ~(size_t)15;
-    s.dq = reinterpret_cast<DPConst*>(base + b); b += (size_t)ng * sizeof(DPConst);
-    s.pI = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * sizeof(double);
-    s.pI2 = reinterpret_cast<double*>(base + b); b += (size_t)pfx_len(K) * sizeof(double);
-    s.jlo = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
-    s.jf = reinterpret_cast<short*>(base + b); b += (size_t)K * sizeof(short);
-    s.jw = reinterpret_cast<short*>(base + b); b += (size_t)kWarps * K * sizeof(short);
-    b = (b + 15) & ~(size_t)15;
-    s.tinf = reinterpret_cast<double*>(base + b); b += (size_t)ng * sizeof(double);
-    s.red = reinterpret_cast<double*>(base + b); b += 5 * kWarps * sizeof(double);
-    s.sid = reinterpret_cast<long long*>(base + b); b += 2 * sizeof(long long);
-    s.ctl = reinterpret_cast<int*>(base + b); b += 8 * sizeof(int);
-    b = (b + 15) & ~(size_t)15;
-    s.rows = base + b;
+    smem_layout(base, K, ng, rec, &s);
     return s;
 }
 
@@ -1839,7 +1877,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     static_assert(PHASE == 0 || (TILE != 0 && kWarps == 1), "the two-kernel path is the tiled, one-warp CTA");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = C.K, ng = C.ng;
-    const Smem sm = carve_smem(smem_raw, K, ng);
+    // PHASE 2 keeps two prep-record buffers (the current scenario's, the next one's in flight)
+    Smem sm = carve_smem(smem_raw, K, ng, PHASE == 2 ? (int)C.prep_stride : 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int GL = 32 / G;
     const int grp = lane / GL;
@@ -1893,10 +1932,39 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     WorkCount wc{out.work ? s_work + tid * 5 : nullptr};
     __shared__ double s_par[5];              // alpha, c1d, c2d, c1v, c2v of the current scenario
 
+    // backtrack stack of the epilogue: the sort keys (dead after the sort) or, in the DP kernel, the
+    // shared row store / tile buffers (dead after the DPs; >= 2 K bytes); K <= 1024 fits int16
+    short* const bstack = PHASE == 2 ? reinterpret_cast<short*>(sm.rows) : reinterpret_cast<short*>(sm.key);
+    // PHASE 2: the record of the next scenario is fetched by a TMA bulk copy while this one is solved
+    int rcur = 0;
+    unsigned rphase = 0u;
+    auto fetch_rec = [&](int buf) {          // tid 0: take the next queue item, start its record copy
+        const unsigned long long it = atomicAdd(ws.next + BIG, 1ULL);
+        const long long sn = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
+        sm.sid[1] = sn;
+        if (sn >= 0)
+            bulk_load(sm.rec + (size_t)buf * C.prep_stride, ws.prep + (size_t)sn * C.prep_stride,
+                      (unsigned)C.prep_stride, sm.rbar + buf);
+    };
+    if constexpr (PHASE == 2) {
+        if (tid == 0) {
+            mbar_init(sm.rbar, 1);
+            mbar_init(sm.rbar + 1, 1);
+            fence_mbar_init();
+            fetch_rec(0);
+        }
+        __syncthreads();
+    }
+
     for (;;) {
         if (tid == 0) {
-            const unsigned long long it = atomicAdd(ws.next + (PHASE == 1 ? 2 : BIG), 1ULL);
-            sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
+            if constexpr (PHASE == 2) {
+                sm.sid[0] = sm.sid[1];
+                if (sm.sid[0] >= 0) fetch_rec(rcur ^ 1);
+            } else {
+                const unsigned long long it = atomicAdd(ws.next + (PHASE == 1 ? 2 : BIG), 1ULL);
+                sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
+            }
             sm.ctl[0] = 0;
             s_ovf = false;
             s_best = dinf();
@@ -1943,8 +2011,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     const double sk = log2(1.0 + pk[r] * gk[r] / C.sigma2);
                     if (uniform) {
                         tc = fmax(tc, C.lambda * Ikd / ((1.0 / K) * C.Bw * sk));
-                    } else {
-                        tc += C.lambda * Ikd / (C.Bw * sk);
+                    } else {                      // t*_com = (lambda / B_w) sum_k I_k / s_k: one division per task
                         u[r] = Ikd / sk;
                         q += u[r];
                     }
@@ -1958,10 +2025,13 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 s1 += __shfl_xor_sync(0xffffffffu, s1, o);
                 s2 += __shfl_xor_sync(0xffffffffu, s2, o);
             }
-            if (out.w && k0 < K)
+            if (!uniform) tc = (C.lambda / C.Bw) * q;
+            if (out.w && k0 < K) {
+                const double rq = 1.0 / q;
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                    out.w[s * K + k0 + r] = bad ? dnan() : uniform ? 1.0 / K : u[r] / q;
+                    out.w[s * K + k0 + r] = bad ? dnan() : uniform ? 1.0 / K : u[r] * rq;
+            }
             __syncwarp();
         } else {
         #pragma unroll 1
@@ -2231,8 +2301,16 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             continue;
         }
         } else {
-            // ---- PHASE 2: the prep record of scenario s -> shared memory
-            const PrepView pv = prep_view(ws.prep + (size_t)s * C.prep_stride, K, ng);
+            // ---- PHASE 2: scenario s's prep record, already in shared memory (or arriving) -- used in place
+            mbar_wait(sm.rbar + rcur, (rphase >> rcur) & 1u);
+            rphase ^= 1u << rcur;
+            const PrepView pv = prep_view(sm.rec + (size_t)rcur * C.prep_stride, K, ng);
+            rcur ^= 1;
+            sm.Is = pv.Is;
+            sm.jlo = pv.jlo;
+            sm.pI = pv.pI;
+            sm.pI2 = pv.pI2;
+            sm.glb = pv.glb;
             const int fl = pv.flags[0];
             bad = fl & 1;
             bad_alpha = (fl & 2) != 0;
@@ -2241,18 +2319,10 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 __syncthreads();
                 continue;
             }
-            #pragma unroll 1
-            for (int k = tid; k < K; k += kThreads) {
-                sm.Is[k] = pv.Is[k];
-                sm.jlo[k] = pv.jlo[k];
-            }
-            #pragma unroll 1
-            for (int k = tid; k < pfx_len(K); k += kThreads) { sm.pI[k] = pv.pI[k]; sm.pI2[k] = pv.pI2[k]; }
             const double c1d = in.coeffs ? in.coeffs[4 * s] : C.c1d, c2d = in.coeffs ? in.coeffs[4 * s + 1] : C.c2d;
             const double c1v = in.coeffs ? in.coeffs[4 * s + 2] : C.c1v, c2v = in.coeffs ? in.coeffs[4 * s + 3] : C.c2v;
             #pragma unroll 1
             for (int gi = tid; gi < ng; gi += kThreads) {
-                sm.glb[gi] = pv.glb[gi];
                 const int N = pv.N[gi];
                 sm.nq[gi] = N;
                 sm.dq[gi] = make_dpconst(C, C.gmin + gi, pv.L[gi], N, c1d, c2d, c1v, c2v);
@@ -2437,8 +2507,8 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             if (st == 0) {
                 const short* S = Scta + (size_t)gbest * K;
                 int i = K;
-                int* stk = reinterpret_cast<int*>(sm.key);          // the sort keys are dead: a stack
-                while (i > 0) { stk[M++] = i; i = S[i - 1] - 1; }
+                short* stk = bstack;                                  // dead scratch: a stack
+                while (i > 0) { stk[M++] = (short)i; i = S[i - 1] - 1; }
                 lat[0] = Tcom + best; lat[1] = Tcom; lat[2] = best;
                 out.gamma[s] = pbg ? (int)Scta[(size_t)ng * K + K - 1] : C.gmin + gbest;   // pbg: the last batch's
             } else {
@@ -2458,12 +2528,12 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
         #pragma unroll 1
         for (int k = tid; k < K; k += kThreads) {
             if (PHASE != 2) out.order[s * K + k] = sm.ord[k];
-            out.bend[s * K + k] = k < M ? reinterpret_cast<const int*>(sm.key)[M - 1 - k] : 0;
+            out.bend[s * K + k] = k < M ? bstack[M - 1 - k] : 0;
         }
         if (out.bgam)                        // each batch's gamma (gamma* for all unless per-batch)
             #pragma unroll 1
             for (int k = tid; k < K; k += kThreads)
-                out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + reinterpret_cast<const int*>(sm.key)[M - 1 - k] - 1]
+                out.bgam[s * K + k] = k >= M ? 0 : pbg ? (int32_t)Scta[(size_t)ng * K + bstack[M - 1 - k] - 1]
                                                        : C.gmin + sm.ctl[4];
         if (out.trace) {                     // S vector of gamma* (row choices; 0 unless status 0)
             const short* S = Scta + (size_t)max(sm.ctl[4], 0) * K;
@@ -2969,6 +3039,9 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     // the prep kernel does not depend on the row store: one instantiation serves TILE 1 and 2
     KFn k_prep = TILE ? solve_kernel<R, ALGO, 0, G, 1, 1> : k_main;
     const size_t sb_prep = smem_bytes<R, G>(C.K, C.ng, 0, 0);
+    C.prep_stride = TILE ? (long long)prep_stride(C.K, C.ng) : 0;
+    if (TILE) sb = smem_bytes<R, G>(C.K, C.ng, C.rows_in_smem, TILE == 1, TILE == 2 ? rs_pad(C.K, 32 / G) : 0,
+                                    (int)C.prep_stride) + (C.pool_smem ? (pool_bytes<R>(C.pool_cap_smem) + 15) & ~(size_t)15 : 0);
     CU(cudaFuncSetAttribute(k_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     CU(cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     int occ_prep = 0;
@@ -2977,7 +3050,7 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_prep, k_prep, kThreads, sb_prep));
         if (occ_prep < 1) return fail(-1, "prep kernel does not fit on an SM");
     }
-    C.prep_stride = TILE ? (long long)prep_stride(C.K, C.ng) : 0;
+    if (sb > (size_t)max_smem) return fail(-1, "shared memory requirement exceeds the device limit");
     int occ = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_main, kThreads, sb));
     if (occ < 1) return fail(-1, "kernel does not fit on an SM");
@@ -3381,6 +3454,14 @@ int sdedge_ipc_open(const void* handle, uint64_t offset, void** dev_ptr)
     void* base = nullptr;
     CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
     *dev_ptr = static_cast<unsigned char*>(base) + offset;
+    return 0;
+}
+
+int sdedge_copy_async(void* dst, const void* src, uint64_t bytes, void* stream)
+{
+    g_err[0] = 0;
+    if ((!dst || !src) && bytes) return fail(-1, "null argument");
+    if (bytes) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
     return 0;
 }
 

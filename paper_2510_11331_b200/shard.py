@@ -59,6 +59,14 @@ class GatherLayout:
             out["w"] = None
         return out
 
+    def chunk_copies(self, base: int, s0: int, local: "GatherLayout", base_local: int, c0: int, c1: int):
+        """(dst, src, bytes) of every array for scenarios [c0, c1) of a rank whose shard starts at
+        s0 of this (cuda:0) layout and lives in `local` at base_local -- one contiguous block
+        per array, for the copy engines."""
+        for (name, off_g, item, wd), (name_l, off_l, _, _) in zip(self.arrays(), local.arrays()):
+            assert name == name_l
+            yield (base + off_g + (s0 + c0) * wd * item, base_local + off_l + c0 * wd * item, (c1 - c0) * wd * item)
+
     def rows(self, base: int, s0: int):
         """Raw-address outputs starting at scenario s0 of a (peer-mapped) buffer."""
         from . import Rows

@@ -22,15 +22,16 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("cfg,n,prec", [("C4", 200_000, 0), ("C3", 100_000, 1)])
-def test_gather_byte_identical(cfg, n, prec):
+@pytest.mark.parametrize("cfg,n,prec,gather", [("C4", 200_000, 0, "chunked"), ("C4", 200_000, 0, "fused"),
+                                               ("C3", 100_003, 1, "chunked")])
+def test_gather_byte_identical(cfg, n, prec, gather):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     ws = min(torch.cuda.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ws}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--config", cfg, "--n", str(n),
-           "--precision", str(prec)]
+           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--config", cfg, "--scenarios", str(n),
+           "--precision", str(prec), "--gather", gather]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-4000:]

@@ -29,8 +29,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C4")
     ap.add_argument("--pair", default=None)
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--scenarios", type=int, default=1_000_000)
     ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--gather", choices=["fused", "chunked"], default="fused")
+    ap.add_argument("--chunks", type=int, default=4)
     a = ap.parse_args()
     ws, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -38,10 +40,10 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     pd, _, _ = scengen.config(a.config, 0, 1, pair=a.pair)
     K = pd["K"]
-    s0, s1 = shard_range(a.n, ws, rank)
+    s0, s1 = shard_range(a.scenarios, ws, rank)
     _, sc, _ = scengen.config(a.config, s0, s1, pair=a.pair)
     t = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).to(dev) for k in ("I", "p", "g", "alpha")}
-    lay = GatherLayout(a.n, K, True)
+    lay = GatherLayout(a.scenarios, K, True)
     if rank == 0:
         buf = torch.full((lay.nbytes,), 0xAB, dtype=torch.uint8, device=dev)   # poison: unwritten rows show
         h = [sd.ipc_export(buf)]
@@ -55,13 +57,32 @@ def main():
         peer = (sd.ipc_open(*h[0]), h[0][1])
         out = lay.rows(peer[0], s0)
     dist.barrier()
-    sd.solve(pd, t["I"], t["p"], t["g"], t["alpha"], None, out=out, precision=a.precision)
+    if a.gather == "fused" or rank == 0:
+        sd.solve(pd, t["I"], t["p"], t["g"], t["alpha"], None, out=out, precision=a.precision)
+    else:                                   # chunked solves, copy engines move each chunk to cuda:0
+        n = s1 - s0
+        loc = GatherLayout(n, K, True)
+        lbuf = torch.empty(loc.nbytes, dtype=torch.uint8, device=dev)
+        lv = loc.views(torch, lbuf)
+        st, cs = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+        for c in range(a.chunks):
+            c0, c1 = n * c // a.chunks, n * (c + 1) // a.chunks
+            if c1 <= c0:
+                continue
+            sd.solve(pd, t["I"][c0:c1], t["p"][c0:c1], t["g"][c0:c1], t["alpha"][c0:c1], None,
+                     out={k: v[c0:c1] for k, v in lv.items() if v is not None}, precision=a.precision)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cs.wait_event(ev)
+            for dst, src, nb in lay.chunk_copies(peer[0], s0, loc, lbuf.data_ptr(), c0, c1):
+                sd.copy_async(dst, src, nb, cs)
+        st.wait_stream(cs)
     torch.cuda.synchronize()
     dist.barrier()
     ok, res = True, {}
     if rank == 0:
         g = lay.views(torch, buf)
-        _, full, _ = scengen.config(a.config, 0, a.n, pair=a.pair)
+        _, full, _ = scengen.config(a.config, 0, a.scenarios, pair=a.pair)
         f = {k: torch.from_numpy(np.ascontiguousarray(full[k])).to(dev) for k in ("I", "p", "g", "alpha")}
         ref = sd.solve(pd, f["I"], f["p"], f["g"], f["alpha"], None, precision=a.precision)
         torch.cuda.synchronize()
@@ -70,10 +91,11 @@ def main():
                                     ref[k].view(torch.uint8)))
             res[k] = same
             ok &= same
-        print(json.dumps({"check": "multi_gpu_gather_byte_identity", "world_size": ws, "n": a.n,
+        print(json.dumps({"check": "multi_gpu_gather_byte_identity", "world_size": ws, "n": a.scenarios,
                           "config": a.config, "pair": a.pair or "default", "precision": a.precision,
+                          "gather": a.gather,
                           "arrays_identical": res, "ok": ok,
-                          "shards": [list(shard_range(a.n, ws, r)) for r in range(ws)]}), flush=True)
+                          "shards": [list(shard_range(a.scenarios, ws, r)) for r in range(ws)]}), flush=True)
     dist.barrier()
     if peer is not None:
         sd.ipc_close(*peer)
