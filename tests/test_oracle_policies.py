@@ -317,3 +317,47 @@ def test_t_inf_at_least_draft_work(orc, pair):
             assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
             n_tight += lb > 0.6 * t_inf
     assert n_tight > 0 or pair == "68M-7B"
+
+
+@pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
+def test_t_inf_at_least_verify_work_by_batch_count(orc, pair):
+    """T_inf(gamma) >= min over the batch count M of the verify stage's serial work: M = 1 is
+    sum_n T^v_n(K, I_K), M = 2 the best split into two memory-feasible batches (each padded to its
+    last, longest task), M >= 3 at least every task's own verify slope plus 3 intercepts
+    (eq:time: each step's makespan >= sum_m T^v_{n,m}; eq:flops_v, eq:latency_b2).  The GPU
+    uses it to skip a gamma before its DP; pinned on the literal DP, with a
+    binding memory window for the 1.1B draft."""
+    K = 10
+    pd = scengen.params(pair, K=K, gamma_min=1, gamma_max=8, O_max=160)
+    if pair == "1.1B-7B":
+        J, h1, h2 = scengen.MODELS["1.1B"]
+        pd = dict(pd, mem_capacity_bytes=orc.param_memory(J, h1, h2) + 6 * orc.kv_memory_per_task(J, h1, 300, 160))
+    sc = scengen.generate(97, K, 0, 6)
+    n_bind = 0
+    for s in range(6):
+        Is = np.sort(sc["I"][s])
+        alpha = float(sc["alpha"][s])
+        for gamma in (1, 2, 5):
+            L = orc.expected_tokens(alpha, gamma)
+            N = orc.decode_steps(pd["O_max"], L)
+            t_inf = orc.dp(pd, Is, alpha, gamma)[0]
+            if not np.isfinite(t_inf):
+                continue
+
+            def vwork(b, I):           # sum_n T^v_n of one batch of b tasks padded to I
+                return sum(orc.verify_time(pd, b, int(I), gamma, L, n) for n in range(1, N + 1))
+
+            def fits(b, I):
+                return np.isfinite(orc.eval_plan(dict(pd, K=b), np.full(b, I, np.int32), alpha, gamma, [b]))
+            own = sum(vwork(2, I) - vwork(1, I) for I in Is)
+            vc = 2 * vwork(1, Is[-1]) - vwork(2, Is[-1])
+            cands = [own + 3 * vc]
+            if fits(K, Is[-1]):
+                cands.append(vwork(K, Is[-1]))
+            for sp in range(1, K):
+                if fits(sp, Is[sp - 1]) and fits(K - sp, Is[-1]):
+                    cands.append(vwork(sp, Is[sp - 1]) + vwork(K - sp, Is[-1]))
+            lb = min(cands)
+            assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
+            n_bind += lb > own + vc
+    assert n_bind > 0
