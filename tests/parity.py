@@ -101,7 +101,8 @@ def compare(pd: dict, sc: dict, gpu: dict, orc: dict, precision: int = 0, orc_mo
         if pol == 6:                      # per-batch gamma: every batch's gamma is part of the schedule
             same = same and np.array_equal(gpu["batch_gamma"][s], orc["batch_gamma"][a])
         if same:
-            r = np.abs(lg - lo) / np.abs(lo)
+            with np.errstate(divide="ignore", invalid="ignore"):
+                r = np.where(lg == lo, 0.0, np.abs(lg - lo) / np.abs(lo))
             worst = max(worst, float(r.max()))
             if r.max() > tol["rel"]:
                 fails.append(f"s={s}: latency rel err {r.max():.3e} (gpu {lg}, oracle {lo})")
