@@ -108,9 +108,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
-    ap.add_argument("--gather", choices=["chunked", "fused"], default="chunked",
+    ap.add_argument("--gather", choices=["auto", "chunked", "fused"], default="auto",
                     help="multi-GPU gather: chunked solves + copy-engine peer copies overlapped with the next "
-                         "chunk's solve, or the kernels' own peer stores")
+                         "chunk's solve, or the kernels' own peer stores; auto = fused up to 2 GPUs, chunked "
+                         "above (measured: r2p4)")
     ap.add_argument("--gather-chunks", type=int, default=6)
     ap.add_argument("--batching-policy", type=int, default=0,
                     help="0 proposed (Algorithm 1), 1 SD w/o pipeline, 2-5 paper baselines, 6 per-batch gamma")
@@ -270,6 +271,8 @@ def main():
     from paper_2510_11331_b200.shard import GatherLayout, shard_range
 
     ws, rank, local = dist_env()
+    if args.gather == "auto":
+        args.gather = "fused" if ws <= 2 else "chunked"
     torch.cuda.set_device(local)
     if ws > 1:
         # NCCL may print its version banner on stdout when the communicator is

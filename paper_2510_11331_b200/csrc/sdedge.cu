@@ -103,6 +103,12 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 constexpr int kThreads = kWarps * 32;
 
 // ------------------------------------------------------------ call constants
+// Byte offsets of the shared-memory arrays of one CTA (computed on the host by smem_layout, so that
+// the kernel forms each array address as base + constant instead of re-deriving the layout)
+struct SmemOff {
+    unsigned I, Is, ord, key, glb, gord, nq, dq, pI, pI2, jlo, jf, jw, tinf, red, sid, ctl, rows, rec, rbar;
+};
+
 struct Consts {
     int K, O_max, gmin, ng;
     int Jd, hd, h2d, Jv, hv, h2v;
@@ -116,6 +122,7 @@ struct Consts {
     long long rows_stride;               // bytes of one warp's global row state
     long long ybuf_stride;               // doubles of one CTA's per-batch-gamma rows, (K+1) x 2 x O_max
     long long prep_stride;               // bytes of one scenario's prep record (two-kernel path)
+    SmemOff so;                          // shared layout of this launch's kernel (PHASE 0/2; set per launch)
     int pool_smem;                       // first-pass envelope pool in shared memory (TILE == 2)
     long long pool_cap_smem;             // its capacity in segments
 };
@@ -668,88 +675,84 @@ __host__ __device__ inline int sort_len(int K)
     return p;
 }
 
-// Shared-memory layout of one CTA (carve when s != nullptr, else just size it).  rec > 0 is the DP
+// Shared-memory layout of one CTA: offsets of every array and the total size.  rec > 0 is the DP
 // kernel of the two-kernel path: it keeps two prep-record buffers of rec bytes (the current
 // scenario's and the prefetched next one's, filled by TMA bulk copies) and points Is, jlo, pI, pI2
 // and glb into them, so it has no arrays of its own for those (nor for I, ord and the sort keys).
-__host__ __device__ inline size_t smem_layout(unsigned char* base, int K, int ng, int rec, Smem* s)
+// Arrays a kernel does not have get offset 0xffffffff.
+__host__ __device__ inline size_t smem_layout(int K, int ng, int rec, SmemOff* o)
 {
     size_t b = 0;
-    auto at = [&](size_t bytes, size_t align) -> unsigned char* {
+    auto at = [&](size_t bytes, size_t align) -> unsigned {
         b = (b + align - 1) & ~(align - 1);
-        unsigned char* p = base ? base + b : nullptr;
+        const unsigned off = (unsigned)b;
         b += bytes;
-        return p;
+        return off;
     };
+    const unsigned none = 0xffffffffu;
+    SmemOff t;
     if (rec > 0) {
-        unsigned char* r0 = at((size_t)2 * rec, 16);
-        unsigned char* bars = at(2 * sizeof(unsigned long long), 8);
-        if (s) {
-            s->rec = r0;
-            s->rbar = reinterpret_cast<unsigned long long*>(bars);
-            s->I = s->Is = s->ord = nullptr;
-            s->key = nullptr;
-        }
+        t.rec = at((size_t)2 * rec, 16);
+        t.rbar = at(2 * sizeof(unsigned long long), 8);
+        t.I = t.Is = t.ord = t.key = none;
     } else {
-        unsigned char* pI_ = at((size_t)K * sizeof(int), 16);
-        unsigned char* pIs = at((size_t)K * sizeof(int), 4);
-        unsigned char* pord = at((size_t)K * sizeof(int), 4);
-        unsigned char* pkey = at((size_t)sort_len(K) * sizeof(unsigned long long), 16);
-        if (s) {
-            s->I = reinterpret_cast<int*>(pI_);
-            s->Is = reinterpret_cast<int*>(pIs);
-            s->ord = reinterpret_cast<int*>(pord);
-            s->key = reinterpret_cast<unsigned long long*>(pkey);
-            s->rec = nullptr;
-            s->rbar = nullptr;
-        }
+        t.I = at((size_t)K * sizeof(int), 16);
+        t.Is = at((size_t)K * sizeof(int), 4);
+        t.ord = at((size_t)K * sizeof(int), 4);
+        t.key = at((size_t)sort_len(K) * sizeof(unsigned long long), 16);
+        t.rec = t.rbar = none;
     }
-    unsigned char* pglb = rec > 0 ? nullptr : at((size_t)ng * sizeof(double), 8);
-    unsigned char* pgord = at((size_t)ng * sizeof(int), 4);
-    unsigned char* pnq = at((size_t)ng * sizeof(int), 4);
-    unsigned char* pdq = at((size_t)ng * sizeof(DPConst), 16);
-    unsigned char* ppI = rec > 0 ? nullptr : at((size_t)pfx_len(K) * sizeof(double), 8);
-    unsigned char* ppI2 = rec > 0 ? nullptr : at((size_t)pfx_len(K) * sizeof(double), 8);
-    unsigned char* pjlo = rec > 0 ? nullptr : at((size_t)K * sizeof(short), 2);
-    unsigned char* pjf = at((size_t)K * sizeof(short), 2);
-    unsigned char* pjw = at((size_t)kWarps * K * sizeof(short), 2);
-    unsigned char* ptinf = at((size_t)ng * sizeof(double), 16);
-    unsigned char* pred = at(5 * kWarps * sizeof(double), 8);
-    unsigned char* psid = at(2 * sizeof(long long), 8);
-    unsigned char* pctl = at(8 * sizeof(int), 4);
-    unsigned char* prows = at(0, 16);
-    if (s) {
-        s->glb = reinterpret_cast<double*>(pglb);
-        s->gord = reinterpret_cast<int*>(pgord);
-        s->nq = reinterpret_cast<int*>(pnq);
-        s->dq = reinterpret_cast<DPConst*>(pdq);
-        s->pI = reinterpret_cast<double*>(ppI);
-        s->pI2 = reinterpret_cast<double*>(ppI2);
-        s->jlo = reinterpret_cast<short*>(pjlo);
-        s->jf = reinterpret_cast<short*>(pjf);
-        s->jw = reinterpret_cast<short*>(pjw);
-        s->tinf = reinterpret_cast<double*>(ptinf);
-        s->red = reinterpret_cast<double*>(pred);
-        s->sid = reinterpret_cast<long long*>(psid);
-        s->ctl = reinterpret_cast<int*>(pctl);
-        s->rows = prows;
-    }
+    t.glb = rec > 0 ? none : at((size_t)ng * sizeof(double), 8);
+    t.gord = at((size_t)ng * sizeof(int), 4);
+    t.nq = at((size_t)ng * sizeof(int), 4);
+    t.dq = at((size_t)ng * sizeof(DPConst), 16);
+    t.pI = rec > 0 ? none : at((size_t)pfx_len(K) * sizeof(double), 8);
+    t.pI2 = rec > 0 ? none : at((size_t)pfx_len(K) * sizeof(double), 8);
+    t.jlo = rec > 0 ? none : at((size_t)K * sizeof(short), 2);
+    t.jf = at((size_t)K * sizeof(short), 2);
+    t.jw = at((size_t)kWarps * K * sizeof(short), 2);
+    t.tinf = at((size_t)ng * sizeof(double), 16);
+    t.red = at(5 * kWarps * sizeof(double), 8);
+    t.sid = at(2 * sizeof(long long), 8);
+    t.ctl = at(8 * sizeof(int), 4);
+    t.rows = at(0, 16);
+    if (o) *o = t;
     return (b + 15) & ~(size_t)15;
 }
 
 template <typename R, int G>
 __host__ __device__ inline size_t smem_bytes(int K, int ng, int rows_in_smem, int tile, int row_pad = 0, int rec = 0)
 {
-    size_t b = smem_layout(nullptr, K, ng, rec, nullptr);
+    size_t b = smem_layout(K, ng, rec, nullptr);
     if (rows_in_smem) b += (size_t)kWarps * G * rows_bytes<R>(K + row_pad);
     if (tile) b += (size_t)kWarps * G * tile_bytes<R, G>();
     return b;
 }
 
-__device__ inline Smem carve_smem(unsigned char* base, int K, int ng, int rec = 0)
+__device__ inline Smem carve_smem(unsigned char* base, const SmemOff& o)
 {
+    auto p = [&](unsigned off) -> unsigned char* { return base + off; };   // (absent arrays are never used)
     Smem s;
-    smem_layout(base, K, ng, rec, &s);
+    s.I = reinterpret_cast<int*>(p(o.I));
+    s.Is = reinterpret_cast<int*>(p(o.Is));
+    s.ord = reinterpret_cast<int*>(p(o.ord));
+    s.key = reinterpret_cast<unsigned long long*>(p(o.key));
+    s.glb = reinterpret_cast<double*>(p(o.glb));
+    s.gord = reinterpret_cast<int*>(p(o.gord));
+    s.nq = reinterpret_cast<int*>(p(o.nq));
+    s.dq = reinterpret_cast<DPConst*>(p(o.dq));
+    s.pI = reinterpret_cast<double*>(p(o.pI));
+    s.pI2 = reinterpret_cast<double*>(p(o.pI2));
+    s.jlo = reinterpret_cast<short*>(p(o.jlo));
+    s.jf = reinterpret_cast<short*>(p(o.jf));
+    s.jw = reinterpret_cast<short*>(p(o.jw));
+    s.tinf = reinterpret_cast<double*>(p(o.tinf));
+    s.red = reinterpret_cast<double*>(p(o.red));
+    s.sid = reinterpret_cast<long long*>(p(o.sid));
+    s.ctl = reinterpret_cast<int*>(p(o.ctl));
+    s.rows = p(o.rows);
+    s.rec = p(o.rec);
+    s.rbar = reinterpret_cast<unsigned long long*>(p(o.rbar));
     return s;
 }
 
@@ -1202,6 +1205,37 @@ __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, s
     }
     work_flush(wc, true, n_cand, 0u, n_cand, n_steps, lane == 0 ? rows : 0u);
     return T_last;
+}
+
+// Lower bound of T_inf(gamma) from the verify stage's serial work with the batch count (DESIGN.md
+// 5.2d): it is sum_m (b_m vsl(I_m) + vc) over the plan's batches, so T_inf >= min over M of: M = 1,
+// K vsl(I_K) + vc; M = 2, the best memory-feasible split (each batch padded to its last task); M >= 3,
+// sum_k vsl(I_k) + 3 vc.  vsl(I) = kv I^2 + qb I + qc per unit batch size.  Warp-collective (lanes
+// take split points); evaluated only for a gamma that survived the O(1) bounds, right before its DP.
+__device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
+{
+    const int lane = threadIdx.x & 31;
+    const double c = D.hv2 + D.g;
+    const double qb = D.kv * (2.0 * D.g + D.hv2) + D.Mx * D.kv * (1.0 + D.g);
+    const double qc = D.kv * D.g * c + D.Mx * D.kv * (1.0 + D.g) * c + D.bvc * D.sumM;
+    const double vc = D.c2vv * (D.Mx + 1.0);
+    const int pt = K / kPfx + 1;
+    const double S1 = sm.pI[pt], S2 = sm.pI2[pt], Kd = (double)K;
+    const double own = D.kv * S2 + qb * S1 + Kd * qc;                 // sum_k vsl(I_k)
+    const double IK = (double)sm.Is[K - 1];
+    const double vK = fma(fma(D.kv, IK, qb), IK, qc);
+    double lb = own + 3.0 * vc;                                       // M >= 3
+    if (sm.jlo[K - 1] == 1) lb = fmin(lb, Kd * vK + vc);              // M = 1
+    const int jK = sm.jlo[K - 1];                                     // batch sp+1..K fits iff jK <= sp+1
+    double b2 = dinf();
+    for (int sp = max(jK - 1, 1) + lane; sp < K; sp += 32) {          // M = 2, split after row sp
+        if (sm.jlo[sp - 1] != 1) continue;                            // batch 1..sp must fit
+        const double Isp = (double)sm.Is[sp - 1];
+        b2 = fmin(b2, fma((double)sp, fma(fma(D.kv, Isp, qb), Isp, qc), (double)(K - sp) * vK));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b2 = fmin(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+    return fmin(lb, b2 + 2.0 * vc);
 }
 
 // ------------------------------------------------------------ TMA bulk copies (sm_90+/sm_100a)
@@ -1878,7 +1912,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = C.K, ng = C.ng;
     // PHASE 2 keeps two prep-record buffers (the current scenario's, the next one's in flight)
-    Smem sm = carve_smem(smem_raw, K, ng, PHASE == 2 ? (int)C.prep_stride : 0);
+    Smem sm = carve_smem(smem_raw, C.so);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int GL = 32 / G;
     const int grp = lane / GL;
@@ -2386,9 +2420,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     left &= ~deadm;
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        const int pos = left ? __ffs(left) - 1 : -1;
+                        int pos = left ? __ffs(left) - 1 : -1;
                         if (pos >= 0) left &= left - 1u;
-                        const int sel = __shfl_sync(0xffffffffu, q_l, pos >= 0 ? pos : 0);
+                        int sel = __shfl_sync(0xffffffffu, q_l, pos >= 0 ? pos : 0);
+                        // a gamma that is not the scenario's first DP must also pass the batch-count bound
+                        if constexpr (G == 1 && TILE != 0)
+                            while (pos >= 0 && prune && s_best < dinf() &&
+                                   lb_batches(sm, sm.dq[sel], K) * (1.0 - mg) > s_best * (1.0 + mg)) {
+                                if (lane == 0) sm.tinf[sel] = dinf();
+                                pos = left ? __ffs(left) - 1 : -1;
+                                if (pos >= 0) left &= left - 1u;
+                                sel = __shfl_sync(0xffffffffu, q_l, pos >= 0 ? pos : 0);
+                            }
                         if (g == grp) mine = pos >= 0 ? sel : -1;
                     }
                 } else {
@@ -3098,15 +3141,20 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (n > 0) {
         C.pool_cap = cap_main;
         w.pool = wsb + o_pool;
+        SmemOff so_prep, so_main;
+        smem_layout(C.K, C.ng, 0, &so_prep);
+        smem_layout(C.K, C.ng, TILE ? (int)C.prep_stride : 0, &so_main);
         if (TILE) {
             const long long grid_prep = std::min((long long)nsm * occ_prep, n);
             const int tq = kt_begin(KT_PREP, st);
+            C.so = so_prep;
             k_prep<<<(unsigned)grid_prep, kThreads, sb_prep, st>>>(C, in, out, n, w, 0);
             kt_end(tq, st);
             ++launches;
             CU(cudaGetLastError());
         }
         int tq = kt_begin(KT_MAIN, st);
+        C.so = so_main;
         k_main<<<(unsigned)grid, kThreads, sb, st>>>(C, in, out, n, w, 0);
         kt_end(tq, st);
         ++launches;
