@@ -87,6 +87,9 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_SHFL_ARGMIN
 #define SDEDGE_TILE_SHFL_ARGMIN 1
 #endif
+#ifndef SDEDGE_CHUNK_SKIP
+#define SDEDGE_CHUNK_SKIP 1   // phase A: skip a 16-row chunk whose smallest bound exceeds every lane's threshold
+#endif
 #ifndef SDEDGE_POOL_SMEM
 #define SDEDGE_POOL_SMEM 0    // 1: first-pass envelope pool in shared memory for draft-bound pairs (measured slower: 4.12 vs 4.33 M/s, r2k)
 #endif
@@ -1670,7 +1673,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             // are non-decreasing in p (5.2d), so every predecessor of the chunk has key >= key[a] and
             // batch size >= i - (e-1): LB1 >= key[a] + (i-e+1) vsl + vc.  A chunk whose bound exceeds
             // every lane's threshold (key[a] shaded by 1e-13, fp32 1e-6, against rounding) is skipped
-            if (mono) {
+            if (SDEDGE_CHUNK_SKIP && mono) {
                 const R ka = buf[0].key * (sizeof(R) == 8 ? (R)(1.0 - 1e-13) : (R)(1.0 - 1e-6));
                 const R lbc = ka + (R)fma(bda - (double)(e - a - 1), rc.vsl, rc.vc);
                 if (__all_sync(0xffffffffu, !own || lbc > thr)) {
