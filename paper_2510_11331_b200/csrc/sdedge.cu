@@ -1228,17 +1228,32 @@ __device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
     const double IK = (double)sm.Is[K - 1];
     const double vK = fma(fma(D.kv, IK, qb), IK, qc);
     double lb = own + 3.0 * vc;                                       // M >= 3
-    if (sm.jlo[K - 1] == 1) lb = fmin(lb, Kd * vK + vc);              // M = 1
+    if (sm.jlo[K - 1] == 1 && Kd * vK + vc < lb) lb = Kd * vK + vc;    // M = 1
     const int jK = sm.jlo[K - 1];                                     // batch sp+1..K fits iff jK <= sp+1
-    double b2 = dinf();
-    for (int sp = max(jK - 1, 1) + lane; sp < K; sp += 32) {          // M = 2, split after row sp
-        if (sm.jlo[sp - 1] != 1) continue;                            // batch 1..sp must fit
-        const double Isp = (double)sm.Is[sp - 1];
-        b2 = fmin(b2, fma((double)sp, fma(fma(D.kv, Isp, qb), Isp, qc), (double)(K - sp) * vK));
-    }
+    // M = 2, split after row sp: four independent split points per lane per iteration (ILP)
+    const double inf = dinf();
+    double b2[4] = {inf, inf, inf, inf};
+    for (int sp0 = max(jK - 1, 1) + lane; sp0 < K; sp0 += 128) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) b2 = fmin(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-    return fmin(lb, b2 + 2.0 * vc);
+        for (int u = 0; u < 4; ++u) {
+            const int sp = sp0 + 32 * u;
+            if (sp < K && sm.jlo[sp - 1] == 1) {                      // batch 1..sp must fit
+                const double Isp = (double)sm.Is[sp - 1];
+                const double v = fma((double)sp, fma(fma(D.kv, Isp, qb), Isp, qc), (double)(K - sp) * vK);
+                b2[u] = v < b2[u] ? v : b2[u];
+            }
+        }
+    }
+    double m2 = b2[0] < b2[1] ? b2[0] : b2[1];
+    const double m3 = b2[2] < b2[3] ? b2[2] : b2[3];
+    m2 = m3 < m2 ? m3 : m2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, m2, o);
+        m2 = ov < m2 ? ov : m2;
+    }
+    const double lb2 = m2 + 2.0 * vc;
+    return lb2 < lb ? lb2 : lb;
 }
 
 // ------------------------------------------------------------ TMA bulk copies (sm_90+/sm_100a)
@@ -2532,6 +2547,19 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
 
 
         // ---- gamma* (smallest argmin, reading A7) and backtrack (reading A5)
+        double wbest = dinf();
+        int wg = -1;
+        if (kWarps == 1 && ng <= 32 && !pbg) {   // one warp: the argmin as a butterfly (ties -> smaller gamma)
+            if (lane < ng) { wbest = sm.tinf[lane]; wg = wbest < dinf() ? lane : -1; }
+            if (wg < 0) wg = 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, wbest, o);
+                const int og = __shfl_xor_sync(0xffffffffu, wg, o);
+                if (ob < wbest || (ob == wbest && og < wg)) { wbest = ob; wg = og; }
+            }
+            if (wg == 0x7fffffff) wg = -1;
+        }
         if (tid == 0) {
             int st = 0, gbest = -1, M = 0;
             double best = dinf();
@@ -2541,6 +2569,10 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             else if (pbg) {
                 best = sm.tinf[0];
                 gbest = best < dinf() ? 0 : -1;
+                if (gbest < 0) st = 1;
+            } else if (kWarps == 1 && ng <= 32) {
+                best = wbest;
+                gbest = wg;
                 if (gbest < 0) st = 1;
             } else {
                 #pragma unroll 1
