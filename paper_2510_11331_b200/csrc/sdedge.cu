@@ -1210,10 +1210,13 @@ __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, s
     return T_last;
 }
 
-// Lower bound of T_inf(gamma) from the verify stage's serial work with the batch count (DESIGN.md
-// 5.2d): it is sum_m (b_m vsl(I_m) + vc) over the plan's batches, so T_inf >= min over M of: M = 1,
-// K vsl(I_K) + vc; M = 2, the best memory-feasible split (each batch padded to its last task); M >= 3,
-// sum_k vsl(I_k) + 3 vc.  vsl(I) = kv I^2 + qb I + qc per unit batch size.  Warp-collective (lanes
+// Lower bound of T_inf(gamma) from the verify stage's serial work with the batch count, plus the first
+// batch's draft work: in every step the verify stage cannot start before the first batch's
+// draft is done, so T_n >= T^d_{n,1} + sum_m T^v_{n,m}; summed over n the verify part is sum_m (b_m vsl(I_m)
+// + vc).  Hence T_inf >= min over the batch count M of: M = 1, K vsl(I_K) + vc + K dsl(I_K) + dc (the exact
+// single-batch latency); M = 2, the best memory-feasible split s (batches padded to their last task) with
+// s vsl(I_s) + (K-s) vsl(I_K) + 2 vc + s dsl(I_s) + dc; M >= 3, sum_k vsl(I_k) + 3 vc + dsl(I_1) + dc.
+// vsl, dsl are quadratics in I per unit batch size (Appendix A); dc = gamma c2d N.  Warp-collective (lanes
 // take split points); evaluated only for a gamma that survived the O(1) bounds, right before its DP.
 __device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
 {
@@ -1222,13 +1225,21 @@ __device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
     const double qb = D.kv * (2.0 * D.g + D.hv2) + D.Mx * D.kv * (1.0 + D.g);
     const double qc = D.kv * D.g * c + D.Mx * D.kv * (1.0 + D.g) * c + D.bvc * D.sumM;
     const double vc = D.c2vv * (D.Mx + 1.0);
+    // draft slope per unit batch: td1 + Mx ad + sumM bdc (row_coef), 0 at gamma = 0
+    const bool gd = D.g > 0.0;
+    const double da = gd ? D.kd : 0.0;
+    const double db = gd ? D.kd * (D.g - 1.0 + D.hd2 + D.Mx * D.g) : 0.0;
+    const double dcq = gd ? D.kd * ((D.g - 1.0) * D.hd2 + D.tri + D.Mx * (D.g * D.hd2 + D.tri)) + D.sumM * D.bdc : 0.0;
+    const double dc = D.c2dg * (D.Mx + 1.0);
     const int pt = K / kPfx + 1;
     const double S1 = sm.pI[pt], S2 = sm.pI2[pt], Kd = (double)K;
     const double own = D.kv * S2 + qb * S1 + Kd * qc;                 // sum_k vsl(I_k)
-    const double IK = (double)sm.Is[K - 1];
+    const double I1 = (double)sm.Is[0], IK = (double)sm.Is[K - 1];
     const double vK = fma(fma(D.kv, IK, qb), IK, qc);
-    double lb = own + 3.0 * vc;                                       // M >= 3
-    if (sm.jlo[K - 1] == 1 && Kd * vK + vc < lb) lb = Kd * vK + vc;    // M = 1
+    const double dK = fma(fma(da, IK, db), IK, dcq);
+    double lb = own + 3.0 * vc + fma(fma(da, I1, db), I1, dcq) + dc;  // M >= 3
+    const double l1 = Kd * (vK + dK) + vc + dc;                       // M = 1
+    if (sm.jlo[K - 1] == 1 && l1 < lb) lb = l1;
     const int jK = sm.jlo[K - 1];                                     // batch sp+1..K fits iff jK <= sp+1
     // M = 2, split after row sp: four independent split points per lane per iteration (ILP)
     const double inf = dinf();
@@ -1239,7 +1250,8 @@ __device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
             const int sp = sp0 + 32 * u;
             if (sp < K && sm.jlo[sp - 1] == 1) {                      // batch 1..sp must fit
                 const double Isp = (double)sm.Is[sp - 1];
-                const double v = fma((double)sp, fma(fma(D.kv, Isp, qb), Isp, qc), (double)(K - sp) * vK);
+                const double v1 = fma(fma(D.kv, Isp, qb), Isp, qc) + fma(fma(da, Isp, db), Isp, dcq);
+                const double v = fma((double)sp, v1, (double)(K - sp) * vK);
                 b2[u] = v < b2[u] ? v : b2[u];
             }
         }
@@ -1252,7 +1264,7 @@ __device__ double lb_batches(const Smem& sm, const DPConst& D, int K)
         const double ov = __shfl_xor_sync(0xffffffffu, m2, o);
         m2 = ov < m2 ? ov : m2;
     }
-    const double lb2 = m2 + 2.0 * vc;
+    const double lb2 = m2 + 2.0 * vc + dc;
     return lb2 < lb ? lb2 : lb;
 }
 

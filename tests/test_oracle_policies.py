@@ -321,10 +321,11 @@ def test_t_inf_at_least_draft_work(orc, pair):
 
 @pytest.mark.parametrize("pair", ["68M-7B", "1.1B-7B"])
 def test_t_inf_at_least_verify_work_by_batch_count(orc, pair):
-    """T_inf(gamma) >= min over the batch count M of the verify stage's serial work: M = 1 is
-    sum_n T^v_n(K, I_K), M = 2 the best split into two memory-feasible batches (each padded to its
-    last, longest task), M >= 3 at least every task's own verify slope plus 3 intercepts
-    (eq:time: each step's makespan >= sum_m T^v_{n,m}; eq:flops_v, eq:latency_b2).  The GPU
+    """T_inf(gamma) >= min over the batch count M of the verify stage's serial work plus the first
+    batch's draft work: M = 1 is the single batch's latency, M = 2 the best split into two
+    memory-feasible batches (each padded to its last, longest task), M >= 3 at least every task's
+    own verify slope plus 3 intercepts plus a one-task draft at the shortest length (eq:time: each
+    step's makespan >= T^d_{n,1} + sum_m T^v_{n,m}; eq:flops_v, eq:flops_d, eq:latency_b2).  The GPU
     uses it to skip a gamma before its DP; pinned on the literal DP, with a
     binding memory window for the 1.1B draft."""
     K = 10
@@ -347,16 +348,20 @@ def test_t_inf_at_least_verify_work_by_batch_count(orc, pair):
             def vwork(b, I):           # sum_n T^v_n of one batch of b tasks padded to I
                 return sum(orc.verify_time(pd, b, int(I), gamma, L, n) for n in range(1, N + 1))
 
+            def dwork(b, I):           # sum_n T^d_n of one batch (the first batch's draft delays every verify)
+                return sum(orc.draft_time(pd, b, int(I), gamma, L, n) for n in range(1, N + 1))
+
             def fits(b, I):
                 return np.isfinite(orc.eval_plan(dict(pd, K=b), np.full(b, I, np.int32), alpha, gamma, [b]))
             own = sum(vwork(2, I) - vwork(1, I) for I in Is)
             vc = 2 * vwork(1, Is[-1]) - vwork(2, Is[-1])
-            cands = [own + 3 * vc]
+            cands = [own + 3 * vc + dwork(1, Is[0])]
             if fits(K, Is[-1]):
-                cands.append(vwork(K, Is[-1]))
+                cands.append(vwork(K, Is[-1]) + dwork(K, Is[-1]))
+                assert abs(cands[-1] - orc.eval_plan(pd, Is, alpha, gamma, [K])) <= 1e-12 * cands[-1]
             for sp in range(1, K):
                 if fits(sp, Is[sp - 1]) and fits(K - sp, Is[-1]):
-                    cands.append(vwork(sp, Is[sp - 1]) + vwork(K - sp, Is[-1]))
+                    cands.append(vwork(sp, Is[sp - 1]) + vwork(K - sp, Is[-1]) + dwork(sp, Is[sp - 1]))
             lb = min(cands)
             assert t_inf >= lb * (1 - 1e-12), (s, gamma, t_inf, lb)
             n_bind += lb > own + vc
