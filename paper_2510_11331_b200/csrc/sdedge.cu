@@ -117,6 +117,7 @@ struct Consts {
     int Jd, hd, h2d, Jv, hv, h2v;
     double c1d, c2d, c1v, c2v;           // defaults when coeffs == NULL
     double Bw, sigma2, lambda, dl;
+    double isig2;                        // 1 / sigma2
     long long gamma_s, Gp, kvunit;       // Gamma_s, Gamma_p (eq:memory_model), 4 Jd hd
     int bw_policy, batch_policy, static_batch;   // SDEDGE_BW_* / SDEDGE_BATCH_* (paper baselines)
     int flags;                           // SDEDGE_FLAG_*
@@ -488,8 +489,9 @@ __device__ inline DPConst make_dpconst(const Consts& C, int gamma, double L, int
 
 // First feasible batch start j of row i (cons. (b), Alg. 1 lines 10-13): batches of
 // b <= bmax = floor(room / d) tasks fit, room = Gamma_s - Gamma_p, d = 4 Jd hd (I + O_max).
-// Exact integer floor; below 2^52 it is a double division (correctly rounded, so at most one
-// too high) with an exact integer fix-up instead of a 64-bit integer division.
+// Exact integer floor.  Below 2^52 a single-precision estimate q' of room / d (relative error
+// < 2^-21) decides bmax >= i outright when q' >= 2 i + 2; otherwise q < 2^17, so floor(q') is
+// within one of bmax and an exact integer fix-up (products < 2^53, no overflow) finishes it.
 __device__ __noinline__ long long div_slow(long long a, long long b) { return a / b; }
 
 __device__ inline int window_lo(long long room, long long d, int i)
@@ -497,13 +499,43 @@ __device__ inline int window_lo(long long room, long long d, int i)
     long long bmax = 0;
     if (room >= 0 && d > 0) {
         if (room < (1LL << 52) && d < (1LL << 52)) {
-            bmax = (long long)((double)room / (double)d);
+            const float qf = __fdividef((float)room, (float)d);
+            if (qf >= 2.0f * (float)i + 2.0f) return 1;
+            bmax = (long long)qf;
             if (bmax * d > room) --bmax;
+            if ((bmax + 1) * d <= room) ++bmax;
         } else {
             bmax = div_slow(room, d);
         }
     }
     return bmax >= i ? 1 : (int)(i - bmax + 1);
+}
+
+// log2(x) for x >= 1 (x = 1 + p g / sigma^2, eq:opt_w): x = 2^e m, m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh(f) = 2 (f + f^3/3 + ... + f^23/23), f = (m - 1) / (m + 1), |f| <= 0.1716 (the
+// truncated terms < 2^-58 relative); 1/(m+1) by a single-precision seed and two Newton steps.
+// A few ulp from the correctly rounded value (the tolerance on w and T_com is 1e-12 relative).
+__device__ inline double log2_ge1(double x)
+{
+    if (!(x < 1.7976931348623157e308)) return x;               // inf, nan
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    int e = (hi >> 20) - 1023;
+    int mh = (hi & 0x000fffff) | 0x3ff00000;
+    if (mh > 0x3ff6a09e) { mh -= 0x00100000; ++e; }             // m > sqrt(2): m / 2
+    const double m = __hiloint2double(mh, lo);
+    const double num = m - 1.0, den = m + 1.0;                  // both exact
+    double r = (double)__frcp_rn((float)den);
+    r = fma(r, fma(-den, r, 1.0), r);
+    r = fma(r, fma(-den, r, 1.0), r);
+    const double f = num * r, f2 = f * f;
+    double q = 1.0 / 23;
+    q = fma(q, f2, 1.0 / 21); q = fma(q, f2, 1.0 / 19); q = fma(q, f2, 1.0 / 17);
+    q = fma(q, f2, 1.0 / 15); q = fma(q, f2, 1.0 / 13); q = fma(q, f2, 1.0 / 11);
+    q = fma(q, f2, 1.0 / 9);  q = fma(q, f2, 1.0 / 7);  q = fma(q, f2, 1.0 / 5);
+    q = fma(q, f2, 1.0 / 3);
+    const double f2x = 2.0 * f;
+    const double lnm = fma(f2x * f2, q, f2x);
+    return fma(lnm, 1.4426950408889634, (double)e);            // ln m / ln 2 + e
 }
 
 // Warp-register bitonic sort of 32 E 64-bit keys (element e = lane E + r in register r):
@@ -541,14 +573,15 @@ __device__ inline void warp_bitonic(unsigned long long (&x)[E], int lane)
     }
 }
 
-// 32-bit keys (I << 7 | e, valid when 0 <= I < 2^24 and K <= 128): half the shuffles and compares
+// 32-bit keys (I << 7 | e, valid when 0 <= I < 2^24 and K <= 128): half the shuffles and compares;
+// the network is fully unrolled (28 stages at E = 4: distances, directions and registers are constants)
 template <int E>
 __device__ inline void warp_bitonic32(unsigned (&x)[E], int lane)
 {
     constexpr int P = 32 * E;
-#pragma unroll 1
+#pragma unroll
     for (int sz = 2; sz <= P; sz <<= 1) {
-#pragma unroll 1
+#pragma unroll
         for (int st = sz >> 1; st > 0; st >>= 1) {
             if (st >= E) {
 #pragma unroll
@@ -2072,7 +2105,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     const double Ikd = (double)Ik[r];
                     s1 += Ikd;
                     s2 += Ikd * Ikd;
-                    const double sk = log2(1.0 + pk[r] * gk[r] / C.sigma2);
+                    const double sk = log2_ge1(1.0 + pk[r] * gk[r] * C.isig2);
                     if (uniform) {
                         tc = fmax(tc, C.lambda * Ikd / ((1.0 / K) * C.Bw * sk));
                     } else {                      // t*_com = (lambda / B_w) sum_k I_k / s_k: one division per task
@@ -2185,7 +2218,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 const double Ikd = (double)sm.I[k];
                 s1 += Ikd;
                 s2 += Ikd * Ikd;
-                const double sk = log2(1.0 + pg[k] * gg[k] / C.sigma2);
+                const double sk = log2_ge1(1.0 + pg[k] * gg[k] * C.isig2);
                 if (uniform) {
                     const double r = (1.0 / K) * C.Bw * sk;
                     tc = fmax(tc, C.lambda * (double)sm.I[k] / r);
@@ -2272,7 +2305,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 const double L = expected_tokens(s_par[0], gamma);
                 const int N = (int)ceil(__ddiv_rn((double)C.O_max, L));
                 const DPConst D = make_dpconst(C, gamma, L, N, s_par[1], s_par[2], s_par[3], s_par[4]);
-                sm.dq[gi] = D;
+                if (PHASE != 1) sm.dq[gi] = D;      // the prep kernel ships L and N; the DP kernel rebuilds D
                 if (PHASE == 1) sm.tinf[gi] = L;
                 sm.nq[gi] = N;
                 const double c = D.hv2 + D.g;
@@ -3226,7 +3259,7 @@ Consts make_consts(const sdedge_params* p)
     C.Jd = p->draft.layers; C.hd = p->draft.hidden; C.h2d = p->draft.ffn;
     C.Jv = p->verify.layers; C.hv = p->verify.hidden; C.h2v = p->verify.ffn;
     C.c1d = p->c1_draft; C.c2d = p->c2_draft; C.c1v = p->c1_verify; C.c2v = p->c2_verify;
-    C.Bw = p->bandwidth_hz; C.sigma2 = p->noise_w;
+    C.Bw = p->bandwidth_hz; C.sigma2 = p->noise_w; C.isig2 = 1.0 / p->noise_w;
     C.lambda = p->lambda_bits > 0 ? p->lambda_bits : 16.0 * ((double)C.hd + (double)C.hv);
     C.dl = p->downlink_s;
     C.gamma_s = p->mem_capacity_bytes;

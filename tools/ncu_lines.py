@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Warp-stall samples and executed instructions per CUDA source line of one ncu report.
 
-    python tools/ncu_lines.py REPORT.ncu-rep [top]
+    python tools/ncu_lines.py REPORT.ncu-rep [top] [launch index]
 """
 import csv
 import io
@@ -11,7 +11,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, top = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+skip = sys.argv[3] if len(sys.argv) > 3 else "0"
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
+                      "--launch-skip", skip, "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
