@@ -87,6 +87,12 @@ constexpr int kWarps = SDEDGE_WARPS;     // warps per CTA
 #ifndef SDEDGE_TILE_SHFL_ARGMIN
 #define SDEDGE_TILE_SHFL_ARGMIN 1
 #endif
+#ifndef SDEDGE_LBB_FIRST
+#define SDEDGE_LBB_FIRST 0    // 1: the batch-count bound also screens the first gamma of the queue (0: only the later ones)
+#endif
+#ifndef SDEDGE_QCHUNK
+#define SDEDGE_QCHUNK 4       // scenarios taken from the work queue per atomic (persistent CTAs)
+#endif
 #ifndef SDEDGE_CHUNK_SKIP
 #define SDEDGE_CHUNK_SKIP 1   // phase A: skip a 16-row chunk whose smallest bound exceeds every lane's threshold
 #endif
@@ -2035,8 +2041,18 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
     // PHASE 2: the record of the next scenario is fetched by a TMA bulk copy while this one is solved
     int rcur = 0;
     unsigned rphase = 0u;
+    // tid 0 takes queue items SDEDGE_QCHUNK at a time (one atomic round trip per SDEDGE_QCHUNK scenarios)
+    __shared__ unsigned long long s_qnext, s_qend;
+    if (tid == 0) { s_qnext = 0; s_qend = 0; }
+    auto take_item = [&](unsigned long long* ctr) -> unsigned long long {
+        if (s_qnext == s_qend) {
+            s_qnext = atomicAdd(ctr, (unsigned long long)SDEDGE_QCHUNK);
+            s_qend = s_qnext + SDEDGE_QCHUNK;
+        }
+        return s_qnext++;
+    };
     auto fetch_rec = [&](int buf) {          // tid 0: take the next queue item, start its record copy
-        const unsigned long long it = atomicAdd(ws.next + BIG, 1ULL);
+        const unsigned long long it = take_item(ws.next + BIG);
         const long long sn = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
         sm.sid[1] = sn;
         if (sn >= 0)
@@ -2059,7 +2075,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                 sm.sid[0] = sm.sid[1];
                 if (sm.sid[0] >= 0) fetch_rec(rcur ^ 1);
             } else {
-                const unsigned long long it = atomicAdd(ws.next + (PHASE == 1 ? 2 : BIG), 1ULL);
+                const unsigned long long it = take_item(ws.next + (PHASE == 1 ? 2 : BIG));
                 sm.sid[0] = (long long)it < n_items ? (BIG ? ws.ovf_list[it] : (long long)it) : -1;
             }
             sm.ctl[0] = 0;
@@ -2473,6 +2489,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
             const int q_l = lanes_q && lane < ng ? sm.gord[lane] : 0;
             const double glb_l = lanes_q && lane < ng ? sm.glb[q_l] : 0.0;
             unsigned left = lanes_q ? (ng == 32 ? 0xffffffffu : ((1u << ng) - 1u)) : 0u;
+            bool ran = false;                    // a DP of this scenario has finished
             for (;;) {
                 // the next G unpruned gammas of the queue (most promising first)
                 int mine = -1;
@@ -2488,7 +2505,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                         int sel = __shfl_sync(0xffffffffu, q_l, pos >= 0 ? pos : 0);
                         // a gamma that is not the scenario's first DP must also pass the batch-count bound
                         if constexpr (G == 1 && TILE != 0)
-                            while (pos >= 0 && prune && s_best < dinf() &&
+                            while (pos >= 0 && prune && s_best < dinf() && (SDEDGE_LBB_FIRST || ran) &&
                                    lb_batches(sm, sm.dq[sel], K) * (1.0 - mg) > s_best * (1.0 + mg)) {
                                 if (lane == 0) sm.tinf[sel] = dinf();
                                 pos = left ? __ffs(left) - 1 : -1;
@@ -2569,6 +2586,7 @@ solve_kernel(const Consts C, const Inputs in, const Outputs out, long long n, Wo
                     sm.tinf[gi] = t;
                     if (ovf) s_ovf = true;
                 }
+                ran = true;
                 {   // best finished T_inf so far (gamma-level pruning of the later DPs)
                     double tv = (lane % GL == 0 && active) ? t : dinf();
 #pragma unroll
