@@ -690,6 +690,15 @@ struct Smem {
 #define SDEDGE_TILE_CH 16     // rows per TMA chunk of the tiled DP's phase A
 #endif
 constexpr int kTileCh = SDEDGE_TILE_CH;
+#ifndef SDEDGE_DBG
+#define SDEDGE_DBG 0          // 1: event counters of the tiled DP (development builds; sdedge_debug_counters)
+#endif
+#if SDEDGE_DBG
+__device__ unsigned long long g_dbg[16];
+#define DBG_ADD(i, v) atomicAdd(&g_dbg[i], (unsigned long long)(v))
+#else
+#define DBG_ADD(i, v) ((void)0)
+#endif
 
 // per tiled DP: tile rows, two TMA staging buffers, two mbarriers, the DP constants
 template <typename R, int G>
@@ -1821,7 +1830,9 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
         if (own && gl < rend && bj > 0) {
             const int p = bj - 1;
             fin = row_update_rec(rw + p, tb + gl, rw + i, pl, D, rc, (double)(i - p), brest, Mx, top_s, true) == 0;
+            if (SDEDGE_DBG && !fin) DBG_ADD(0, 1);                  // speculation needs the merge path
         }
+        if (SDEDGE_DBG && own && gl < rend && bj <= 0) DBG_ADD(1, 1);   // no phase-A winner
         __syncwarp();
 #if SDEDGE_SPEC >= 2
         // In-tile candidates j = i0+r+1 (predecessor row i0+r, r < gl) are first
@@ -1847,6 +1858,8 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
             if (gl == r && !fin) {           // eq:rg, eq:tt1, eq:tt2 with j* = bj (reading A4)
                 const int p = bj - 1;
                 const RowRec<R>* q = p >= i0 ? tb + (p - i0) : rw + p;
+                if (SDEDGE_DBG) DBG_ADD(3, 1);                               // serial row builds
+                if (SDEDGE_DBG && rw[p].cnt > 0) DBG_ADD(4, rw[p].cnt);
                 if (row_update_rec(q, tb + r, rw + ii, pl, D, rc, (double)(ii - p), brest, Mx, top_s) == 1)
                     ovf_any = true;
                 fin = true;
@@ -1862,6 +1875,7 @@ __device__ double dp_gamma_tiled(const Consts& C, const Smem& sm, RowRec<R>* rw,
                     const R t = env_cand_rec(tb + r, pl, D, rc, (double)(i - ii), Mx, rq, c0);
                     n_full += 1;
                     n_seg += (unsigned)c0;
+                    if (SDEDGE_DBG && t <= bT) DBG_ADD(2, 1);               // an in-tile candidate wins
                     if (t <= bT) { bT = t; thr = prune_thr(bT); bj = ii + 1; brest = rq; fin = false; }   // '<=': largest j
                 }
             }
@@ -3445,6 +3459,15 @@ int host_pipeline(HostPipe& hp, const sdedge_scenarios* s, int64_t n, const sded
 
 // ------------------------------------------------------------ exported C ABI
 extern "C" {
+#if SDEDGE_DBG
+int sdedge_debug_counters(unsigned long long* out)   // development builds: read and clear the event counters
+{
+    unsigned long long z[16] = {};
+    cudaMemcpyFromSymbol(out, g_dbg, sizeof(z));
+    cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+    return 0;
+}
+#endif
 
 int sdedge_abi_version(void) { return SDEDGE_ABI_VERSION; }
 
