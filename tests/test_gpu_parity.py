@@ -261,6 +261,24 @@ def test_permutation_invariance():
     assert np.array_equal(a["gamma"], b["gamma"]) and np.array_equal(a["batch_end"], b["batch_end"])
 
 
+def test_wide_snr_range_bandwidth():
+    """eq:opt_w over SNRs from 1e-14 to 1e14 (the kernel's own log2(1 + SNR) and 1/sigma^2):
+    w* and T_com within 1e-12 of the oracle's libm log2, including SNRs whose 1 + SNR rounds to 1."""
+    pd, sc, _ = scengen.config("C3", 0, 300)
+    rng = np.random.default_rng(11)
+    snr = 10.0 ** rng.uniform(-14, 14, size=sc["g"].shape)
+    snr[:5, 0] = 1e-17                                   # 1 + SNR == 1: s_k = 0, t_com and w* infinite / NaN
+    g = snr * pd["noise_w"] / sc["p"]
+    sc2 = dict(sc, g=np.ascontiguousarray(g))
+    part = lambda a, b: {k: (None if v is None else np.ascontiguousarray(v[a:b])) for k, v in sc2.items()}  # noqa: E731
+    res, _, _ = _check(pd, part(5, 300))
+    assert res["failures"] == 0
+    gg, o = gpu_solve(pd, part(0, 5)), oracle.solve_batch(pd, part(0, 5))
+    for s in range(5):                                    # same non-finite outcome as the oracle
+        assert np.array_equal(np.isfinite(gg["lat"][s]), np.isfinite(o["lat"][s]))
+        assert gg["status"][s] == o["status"][s]
+
+
 def test_streams_and_empty_call():
     import paper_2510_11331_b200 as sd
     pd, sc, _ = scengen.config("C3", 0, 500)
