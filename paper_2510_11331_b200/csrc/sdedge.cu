@@ -130,7 +130,7 @@ struct Consts {
     int rows_in_smem;                    // DP row state in shared (1) or global (0) memory
     long long pool_cap;                  // envelope segments per warp slot
     long long rows_stride;               // bytes of one warp's global row state
-    long long ybuf_stride;               // doubles of one CTA's per-batch-gamma rows, (K+1) x 2 x O_max
+    long long ybuf_stride;               // doubles of one CTA's per-batch-gamma rows, (K+1) x (3 O_max + 1)
     long long prep_stride;               // bytes of one scenario's prep record (two-kernel path)
     SmemOff so;                          // shared layout of this launch's kernel (PHASE 0/2; set per launch)
     int pool_smem;                       // first-pass envelope pool in shared memory (TILE == 2)
@@ -1180,11 +1180,48 @@ __device__ double dp_gamma(const Consts& C, const Smem& sm, RowRec<R>* rw, Pool<
 // max{Upsilon0 + 0, Upsilon1} + 0 = Upsilon1.  Dense, one warp, fp64: the Upsilon rows (n = 1..Nmax,
 // Nmax = max N_gamma) live in a global workspace (row p: Y0[Nmax] then Y1[Nmax]); lanes take steps n,
 // every (j, gamma) candidate is a lane sum + butterfly.  Ties: largest j, then smallest gamma (NB1).
+#ifndef SDEDGE_PBG_WS_GIB
+#define SDEDGE_PBG_WS_GIB 8   // per-batch-gamma row workspace of all CTAs (bounds the grid; one CTA's rows <= 2 GiB)
+#endif
+constexpr long long kPbgWorkspace = (long long)SDEDGE_PBG_WS_GIB << 30;
+
+// Per-(row, gamma) stage constants of the per-batch-gamma DP (hoisted out of the candidate loop)
+struct PbgCoef {
+    double td1, tv1, ad, av, bdc, bvc;   // n = 1 values, n >= 2 intercepts (per unit b, + c2dg / c2vv), slopes in n
+    double c2dg, c2vv;
+    int N;
+};
+
+// Row p of the per-batch-gamma DP in the CTA's workspace: Upsilon0[n], Upsilon1[n] (n = 1..Nmax) and the
+// suffix sums U[k] = sum_{n > k} Upsilon1[n] (k = 0..Nmax): a batch with n_m = N_q < Nmax contributes no
+// stage time after step N_q, so its candidate's steps n > N_q add Upsilon1 of the predecessor unchanged
+// (reading NB1) -- one lookup instead of Nmax - N_q terms.
+__device__ inline void pbg_suffix(double* y1, double* U, int Nmax)
+{
+    const int lane = threadIdx.x & 31;
+    double carry = 0.0;
+    if (lane == 0) U[Nmax] = 0.0;
+    for (int b0 = ((Nmax - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+        const int k = b0 + lane;
+        double v = k < Nmax ? y1[k] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {              // inclusive suffix scan within the block
+            const double t = __shfl_down_sync(0xffffffffu, v, o);
+            if (lane + o < 32) v += t;
+        }
+        if (k < Nmax) U[k] = v + carry;
+        carry += __shfl_sync(0xffffffffu, v, 0);
+    }
+    __syncwarp();
+}
+
 __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, short* S, short* Gm, WorkCount& wc)
 {
     const int lane = threadIdx.x & 31, K = C.K, ng = C.ng;
-    const size_t rs = 2 * (size_t)Nmax;
+    const size_t rs = 3 * (size_t)Nmax + 1;
+    __shared__ PbgCoef s_pc[32];
     for (int n = lane; n < Nmax; n += 32) { Y[n] = 0.0; Y[Nmax + n] = 0.0; }   // row 0 == 0 (reading A3)
+    for (int n = lane; n <= Nmax; n += 32) Y[2 * Nmax + n] = 0.0;
     __syncwarp();
     unsigned n_cand = 0, rows = 0;
     unsigned long long n_steps = 0;
@@ -1193,32 +1230,34 @@ __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, s
         const int jlo = sm.jlo[i - 1];
         if (jlo > i) { T_last = dinf(); break; }
         const int I = sm.Is[i - 1];
+        for (int q = lane; q < ng; q += 32) {          // this row's constants, one gamma per lane
+            const DPConst& D = sm.dq[q];
+            const RowCoef rc = row_coef(D, I);
+            s_pc[q] = PbgCoef{rc.td1, rc.tv1, rc.ad, rc.av, D.bdc, D.bvc, D.c2dg, D.c2vv, sm.nq[q]};
+        }
+        __syncwarp();
         double best = dinf();
         int bj = -1, bq = -1;
         for (int j = jlo; j <= i; ++j) {
             const double b = (double)(i - j + 1);
             const double* y0p = Y + (size_t)(j - 1) * rs;
             const double* y1p = y0p + Nmax;
+            const double* up = y0p + 2 * Nmax;
             for (int q = 0; q < ng; ++q) {
-                const DPConst& D = sm.dq[q];
-                const RowCoef rc = row_coef(D, I);
-                const int Nq = sm.nq[q];
-                const double td1 = fma(b, rc.td1, D.c2dg), tv1 = fma(b, rc.tv1, D.c2vv);
-                const double ad = fma(b, rc.ad, D.c2dg), av = fma(b, rc.av, D.c2vv);
-                const double sd = b * D.bdc, sv = b * D.bvc;
+                const PbgCoef& pc = s_pc[q];
+                const int Nq = pc.N;
+                const double td1 = fma(b, pc.td1, pc.c2dg), tv1 = fma(b, pc.tv1, pc.c2vv);
+                const double ad = fma(b, pc.ad, pc.c2dg), av = fma(b, pc.av, pc.c2vv);
+                const double sd = b * pc.bdc, sv = b * pc.bvc;
                 double acc = 0.0;
-                for (int n = 1 + lane; n <= Nmax; n += 32) {
-                    const double y1 = y1p[n - 1];
-                    if (n <= Nq) {
-                        const double x = (double)(n - 1);
-                        const double td = n == 1 ? td1 : fma(sd, x, ad), tv = n == 1 ? tv1 : fma(sv, x, av);
-                        acc += rmax(y0p[n - 1] + td, y1) + tv;      // eq:t_ij1 (reading A1)
-                    } else {
-                        acc += y1;                                  // batch finished: no stage time
-                    }
+                for (int n = 1 + lane; n <= Nq; n += 32) {
+                    const double x = (double)(n - 1);
+                    const double td = n == 1 ? td1 : fma(sd, x, ad), tv = n == 1 ? tv1 : fma(sv, x, av);
+                    acc += rmax(y0p[n - 1] + td, y1p[n - 1]) + tv;      // eq:t_ij1 (reading A1)
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                acc += up[Nq];                                           // steps after the batch finished
                 if (acc < best || (acc == best && j > bj)) { best = acc; bj = j; bq = q; }   // NB1
             }
             n_cand += (unsigned)ng;
@@ -1226,13 +1265,12 @@ __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, s
         }
         if (bj < 0) { T_last = dinf(); break; }
         {   // eq:tt1 / eq:tt2 with (j*, gamma*)
-            const DPConst& D = sm.dq[bq];
-            const RowCoef rc = row_coef(D, I);
-            const int Nq = sm.nq[bq];
+            const PbgCoef& pc = s_pc[bq];
+            const int Nq = pc.N;
             const double b = (double)(i - bj + 1);
-            const double td1 = fma(b, rc.td1, D.c2dg), tv1 = fma(b, rc.tv1, D.c2vv);
-            const double ad = fma(b, rc.ad, D.c2dg), av = fma(b, rc.av, D.c2vv);
-            const double sd = b * D.bdc, sv = b * D.bvc;
+            const double td1 = fma(b, pc.td1, pc.c2dg), tv1 = fma(b, pc.tv1, pc.c2vv);
+            const double ad = fma(b, pc.ad, pc.c2dg), av = fma(b, pc.av, pc.c2vv);
+            const double sd = b * pc.bdc, sv = b * pc.bvc;
             const double* y0p = Y + (size_t)(bj - 1) * rs;
             double* o0 = Y + (size_t)i * rs;
             for (int n = 1 + lane; n <= Nmax; n += 32) {
@@ -1245,6 +1283,8 @@ __device__ double dp_pbg(const Consts& C, const Smem& sm, double* Y, int Nmax, s
                 o0[n - 1] = y0;
                 o0[Nmax + n - 1] = y1;
             }
+            __syncwarp();
+            pbg_suffix(o0 + Nmax, o0 + 2 * Nmax, Nmax);
         }
         if (lane == 0) {
             S[i - 1] = (short)bj;
@@ -3100,7 +3140,7 @@ int validate(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, const
     if (p->batching_policy == SDEDGE_BATCH_PER_BATCH_GAMMA) {
         if (p->precision != 0) return fail(-1, "per-batch gamma is fp64 only");
         if (p->gamma_max - p->gamma_min + 1 > 32) return fail(-1, "per-batch gamma: at most 32 speculation lengths");
-        if ((long long)(p->K + 1) * 2 * p->O_max * 8 > (2LL << 30)) return fail(-1, "per-batch gamma: (K+1) O_max too large");
+        if ((long long)(p->K + 1) * (3LL * p->O_max + 1) * 8 > (2LL << 30)) return fail(-1, "per-batch gamma: (K+1) O_max too large");
     }
     if (p->batching_policy == SDEDGE_BATCH_STATIC && p->static_batch < 1) return fail(-1, "static_batch < 1");
     if (p->reserved != 0) return fail(-1, "reserved must be 0");
@@ -3211,9 +3251,9 @@ int launch_all(const Consts& C0, const Inputs& in, const Outputs& out, long long
     if (occ < 1) return fail(-1, "kernel does not fit on an SM");
     long long grid = (long long)nsm * occ;
     const bool pbg = C.batch_policy == SDEDGE_BATCH_PER_BATCH_GAMMA;
-    // per-batch gamma: (K+1) Upsilon rows of 2 x Nmax doubles per CTA (Nmax <= O_max); <= 2 GiB in all
-    C.ybuf_stride = pbg ? (long long)(C.K + 1) * 2 * C.O_max : 0;
-    if (pbg) grid = std::max(1LL, std::min(grid, (2LL << 30) / (8 * C.ybuf_stride)));
+    // per-batch gamma: (K+1) Upsilon rows of 3 Nmax + 1 doubles per CTA (Nmax <= O_max); <= SDEDGE_PBG_WS_GIB in all
+    C.ybuf_stride = pbg ? (long long)(C.K + 1) * (3 * (long long)C.O_max + 1) : 0;
+    if (pbg) grid = std::max(1LL, std::min(grid, (kPbgWorkspace) / (8 * C.ybuf_stride)));
     if (grid > n) grid = n;
 
     // typical envelopes have <= a few segments per row: 4 (K+1) + 64 extra
