@@ -141,7 +141,7 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms during the
     timed region (B200_PROFILING.md clocks line)."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -186,14 +186,22 @@ class ClockSampler:
     def summary(self):
         # samples taken inside the timed region (the sampler runs from before the warm-up)
         rows = [r[1:] for r in self.rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        note = None
+        if not rows and self.t0 is not None:
+            # a timed region shorter than the 20 ms sampling period: the samples within 50 ms of it
+            rows = [r[1:] for r in self.rows if self.t0 - 0.05 <= r[0] <= (self.t1 or self.t0) + 0.05]
+            note = "timed region shorter than the sampling period: samples within 50 ms of it"
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[q] for r in rows for q in range(4) if r[3 + q] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "window_s": (self.t1 or 0) - (self.t0 or 0)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(rows), "window_s": (self.t1 or 0) - (self.t0 or 0)}
+        if note:
+            out["note"] = note
+        return out
 
 
 def cpu_model():
