@@ -55,6 +55,7 @@ OPS = {"dense": dict(cand=16, seg=0, step=4, row=40, pruned=0),
 # tools/ncu_traffic.py with the sha256 of csrc/sdedge.cu it was measured on);
 # reported only when that sha matches the source being benchmarked.
 TRAFFIC_JSON = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+L2_BYTES = 126 * 10**6                       # B200 L2 (B200_PROFILING.md)
 
 
 def measured_traffic(key: str):
@@ -374,19 +375,35 @@ def main():
                 sd.copy_async(dst, src, nb, copy_stream)
         stream.wait_stream(copy_stream)
 
+    # inputs of one step: below 2x the 126 MB L2 they could stay cached across steps, so L2 is then
+    # flushed (a 256 MB write) before every timed step, outside that step's events
+    in_bytes = sum(v.numel() * v.element_size() for v in d.values())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if in_bytes < 2 * L2_BYTES else None
+
     def timed(out, count, clk=None):
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step(out, count)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step(out, count)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            el = e0.elapsed_time(e1) * 1e-3
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                step(out, count)
+                b.record(stream)
+            torch.cuda.synchronize()
+            el = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
         if ws > 1:
             dist.barrier()
-        return e0.elapsed_time(e1) * 1e-3
+        return el
 
     uuid = None
     try:
@@ -484,6 +501,9 @@ def main():
                 cpu = {"value": None, "unit": "scenarios/s", "cores": cores, "kind": "oracle",
                        "sample": f"failed: {e}"}
         cfg = config_of(args, n, ws)
+        cfg["l2"] = (f"no flush: inputs per step ({in_bytes / 1e6:.0f} MB) exceed 2x the 126 MB L2" if flush is None else
+                     f"L2 flushed (256 MB write) before every timed step, outside its events; inputs per step "
+                     f"{in_bytes / 1e6:.0f} MB")
         gdesc = ("the solves' own NVLink peer stores into cuda:0's arrays (CUDA IPC)" if args.gather == "fused" else
                  f"{args.gather_chunks} chunked solves of decreasing size per rank, each chunk copied into cuda:0's "
                  f"arrays by the copy engines over NVLink (CUDA IPC) while the next is solved; rank 0 solves "
