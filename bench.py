@@ -441,30 +441,41 @@ def main():
         st = gout["status"] if ws == 1 or not strong else lay.views(torch, gbuf)["status"]
         status_ok = int((st == 0).sum().item())
 
-    # ---- end to end through the host entry point (pinned host in, pinned host out)
+    # ---- end to end through the host entry points (pinned host in, pinned host out): the compact-output
+    # call (the e2e number: same results, uint16 order and a batch-end bit mask, w* in fp64), and the
+    # plain int32 layout for comparison (e2e_full_layout)
     e2e = None
     if not args.no_e2e:
-        hout = sd._alloc_out(torch, n, K, None, True, pin=True)
         ksteps = args.e2e_steps or max(1, min(args.steps, 3))
-        sd.solve_host(pd, host["I"], host["p"], host["g"], host["alpha"], out=hout, stream=stream,
-                      precision=prec, algo=algo)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(ksteps):
-            sd.solve_host(pd, host["I"], host["p"], host["g"], host["alpha"], out=hout, stream=stream,
-                          precision=prec, algo=algo)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        te = max_over_ranks(f0.elapsed_time(f1) * 1e-3, dist, dev)
+
+        def host_rate(call, hout):
+            call(hout)
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(ksteps):
+                call(hout)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            te = max_over_ranks(f0.elapsed_time(f1) * 1e-3, dist, dev)
+            d2h = sum(v.numel() * v.element_size() for v in hout.values() if v is not None)
+            return n_total * ksteps / te, d2h
+
         h2d = sum(v.numel() * v.element_size() for v in host.values())
-        d2h = sum(v.numel() * v.element_size() for v in hout.values() if v is not None)
-        e2e = {"value": n_total * ksteps / te, "unit": "scenarios/s", "h2d_bytes_per_step": h2d * ws,
-               "d2h_bytes_per_step": d2h * ws, "steps": ksteps, "entry": "sdedge_solve_batch_host",
-               "note": "per-rank shard host->device->host; PCIe-bound (inputs alone are 2568 B/scenario)"}
+        rate_c, d2h_c = host_rate(lambda o: sd.solve_host_compact(pd, host["I"], host["p"], host["g"], host["alpha"],
+                                                                  out=o, stream=stream, precision=prec, algo=algo),
+                                  sd.alloc_out_compact(torch, n, K, True))
+        rate_f, d2h_f = host_rate(lambda o: sd.solve_host(pd, host["I"], host["p"], host["g"], host["alpha"], out=o,
+                                                          stream=stream, precision=prec, algo=algo),
+                                  sd._alloc_out(torch, n, K, None, True, pin=True))
+        e2e = {"value": rate_c, "unit": "scenarios/s", "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h_c * ws, "steps": ksteps, "entry": "sdedge_solve_batch_host_compact",
+               "note": "per-rank shard host->device->host, every output of the solve (w* included); order as uint16 "
+                       "and batch ends as a bit mask; PCIe-bound (inputs alone are 2568 B/scenario)",
+               "e2e_full_layout": {"value": rate_f, "d2h_bytes_per_step": d2h_f * ws, "entry": "sdedge_solve_batch_host"}}
 
     # ---- roofline of the dominant kernel (solve_kernel main pass; the second launch
     # is the worst-case-pool pass, empty unless an envelope overflowed)

@@ -166,6 +166,27 @@ int sdedge_solve_batch(const sdedge_scenarios* scenarios, int64_t n, const sdedg
 int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
                             double* out_latency, sdedge_schedule* out_schedule);
 
+/* The same solve on HOST buffers with the schedule re-encoded compactly for the device->host
+ * copy: the copies in both directions share the PCIe link, so fewer output bytes
+ * leave more of it to the inputs.  Same values as sdedge_solve_batch_host, different layout:
+ *   batch_end_mask [n * ceil(K/32)] uint32: bit (e-1) of scenario s's words is set iff a batch ends
+ *                  at sorted position e (the set bits are exactly batch_end[s, 0..M-1]);
+ *   order          [n * K] uint16 (K <= SDEDGE_MAX_K < 2^16): original task index per sorted position;
+ *   gamma, num_batches, status [n] int32 and bw_share [n * K] fp64 (or NULL) as in sdedge_schedule.
+ * Host pointers (pinned memory recommended), asynchronous on params->stream like the host entry;
+ * return codes and per-scenario status as sdedge_solve_batch. */
+typedef struct {
+    int32_t*  gamma;             /* [n]                                   */
+    int32_t*  num_batches;       /* [n]                                   */
+    uint32_t* batch_end_mask;    /* [n * ceil(K/32)]                      */
+    uint16_t* order;             /* [n * K]                               */
+    double*   bw_share;          /* [n * K] or NULL                       */
+    int32_t*  status;            /* [n]                                   */
+} sdedge_compact_schedule;
+
+int sdedge_solve_batch_host_compact(const sdedge_scenarios* scenarios, int64_t n, const sdedge_params* params,
+                                    double* out_latency, sdedge_compact_schedule* out_schedule);
+
 /* Actual-output evaluation of solved schedules (P:316-318,
  * eq:step_n, eq:latency_infer_batch P:519-525, eq:latency_inf).  The planner
  * assumes O_k = O_max; this call replays each scenario's plan

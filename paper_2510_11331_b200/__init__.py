@@ -12,7 +12,7 @@ import os
 
 from ._build import LIB, build  # noqa: F401
 
-__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual", "evaluate_actual", "sdedge_brute_force", "brute_force", "sdedge_pipe_peak", "sdedge_last_error",
+__all__ = ["sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_solve_batch_host_compact", "solve_host_compact", "sdedge_evaluate_actual", "evaluate_actual", "sdedge_brute_force", "brute_force", "sdedge_pipe_peak", "sdedge_last_error",
            "sdedge_last_launch_count", "sdedge_abi_version", "solve", "solve_host", "make_params",
            "ALGO_ENVELOPE", "ALGO_DENSE", "EXPORTED_SYMBOLS", "lib"]
 
@@ -20,10 +20,16 @@ ALGO_ENVELOPE, ALGO_DENSE = 0, 1
 BW_OPTIMAL, BW_UNIFORM = 0, 1
 BATCH_PROPOSED, BATCH_NO_PIPELINE, BATCH_NONE, BATCH_STATIC, BATCH_MAX, BATCH_HEURISTIC, BATCH_PER_BATCH_GAMMA = range(7)
 FLAG_TINY_POOL, FLAG_HEURISTIC_HALF = 1, 2
-EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_evaluate_actual",
+EXPORTED_SYMBOLS = ("sdedge_solve_batch", "sdedge_solve_batch_host", "sdedge_solve_batch_host_compact",
+                    "sdedge_evaluate_actual",
                     "sdedge_brute_force", "sdedge_last_launch_count", "sdedge_last_error",
                     "sdedge_abi_version", "sdedge_pipe_peak", "sdedge_ipc_export", "sdedge_ipc_open",
                     "sdedge_ipc_close", "sdedge_kernel_timing", "sdedge_kernel_times", "sdedge_copy_async")
+
+
+class SdedgeCompactSchedule(C.Structure):
+    _fields_ = [("gamma", C.c_void_p), ("num_batches", C.c_void_p), ("batch_end_mask", C.c_void_p),
+                ("order", C.c_void_p), ("bw_share", C.c_void_p), ("status", C.c_void_p)]
 
 
 class SdedgeModel(C.Structure):
@@ -69,6 +75,9 @@ def lib() -> C.CDLL:
             fn.restype = C.c_int
             fn.argtypes = [C.POINTER(SdedgeScenarios), C.c_int64, C.POINTER(SdedgeParams), C.c_void_p,
                            C.POINTER(SdedgeSchedule)]
+        L.sdedge_solve_batch_host_compact.restype = C.c_int
+        L.sdedge_solve_batch_host_compact.argtypes = [C.POINTER(SdedgeScenarios), C.c_int64, C.POINTER(SdedgeParams),
+                                                      C.c_void_p, C.POINTER(SdedgeCompactSchedule)]
         L.sdedge_evaluate_actual.restype = C.c_int
         L.sdedge_evaluate_actual.argtypes = [C.POINTER(SdedgeScenarios), C.c_void_p, C.c_int64,
                                              C.POINTER(SdedgeParams), C.POINTER(SdedgeSchedule), C.c_void_p]
@@ -183,6 +192,18 @@ def sdedge_solve_batch_host(I, p, g, alpha, coeffs, n, params: SdedgeParams, out
     """Direct C-ABI call on HOST buffers (numpy or pinned torch CPU tensors)."""
     return _call(lib().sdedge_solve_batch_host, I, p, g, alpha, coeffs, n, params, out_latency, gamma,
                  num_batches, batch_end, order, bw_share, status)
+
+
+def sdedge_solve_batch_host_compact(I, p, g, alpha, coeffs, n, params: SdedgeParams, out_latency, gamma,
+                                    num_batches, batch_end_mask, order, bw_share, status):
+    """Direct C-ABI call on HOST buffers with the compact schedule layout (include/sdedge.h)."""
+    sc = SdedgeScenarios(_ptr(I), _ptr(p), _ptr(g), _ptr(alpha), _ptr(coeffs))
+    sch = SdedgeCompactSchedule(_ptr(gamma), _ptr(num_batches), _ptr(batch_end_mask), _ptr(order), _ptr(bw_share),
+                                _ptr(status))
+    rc = lib().sdedge_solve_batch_host_compact(C.byref(sc), n, C.byref(params), _ptr(out_latency), C.byref(sch))
+    if rc != 0:
+        raise RuntimeError(f"sdedge_solve_batch_host_compact failed ({rc}): {sdedge_last_error()}")
+    return rc
 
 
 def sdedge_evaluate_actual(I, p, g, alpha, coeffs, output_len, n, params: SdedgeParams, gamma, num_batches,
@@ -343,6 +364,48 @@ def solve(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream
             _check(f"out[{k}]", v, v.dtype, v.shape, dev)
     sdedge_solve_batch(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end"],
                        o["order"], o["w"], o["status"], work_counters, o.get("trace"), o.get("batch_gamma"))
+    return o
+
+
+def alloc_out_compact(torch, n, K, want_w=True):
+    """Pinned host outputs of sdedge_solve_batch_host_compact."""
+    kw = dict(pin_memory=True)
+    return dict(lat=torch.empty((n, 3), dtype=torch.float64, **kw), gamma=torch.empty(n, dtype=torch.int32, **kw),
+                M=torch.empty(n, dtype=torch.int32, **kw),
+                batch_end_mask=torch.empty((n, (K + 31) // 32), dtype=torch.int32, **kw),   # uint32 bits
+                order=torch.empty((n, K), dtype=torch.int16, **kw),                         # uint16 values
+                w=torch.empty((n, K), dtype=torch.float64, **kw) if want_w else None,
+                status=torch.empty(n, dtype=torch.int32, **kw))
+
+
+def unpack_compact(o) -> dict:
+    """numpy views of a compact result: order as uint16 -> int32, batch_end rebuilt from the mask."""
+    import numpy as np
+    order = o["order"].numpy().view(np.uint16).astype(np.int32)
+    mask = o["batch_end_mask"].numpy().view(np.uint32)
+    n, W = mask.shape
+    K = order.shape[1]
+    bits = ((mask[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(n, W * 32)[:, :K].astype(bool)
+    bend = np.zeros((n, K), np.int32)
+    for s in range(n):
+        e = np.nonzero(bits[s])[0] + 1
+        bend[s, :len(e)] = e
+    return dict(lat=o["lat"].numpy(), gamma=o["gamma"].numpy(), M=o["M"].numpy(), batch_end=bend, order=order,
+                w=None if o["w"] is None else o["w"].numpy(), status=o["status"].numpy())
+
+
+def solve_host_compact(params: dict, I, p, g, alpha, coeffs=None, want_w: bool = True, stream=None, out=None,
+                       precision: int | None = None, algo: int | None = None) -> dict:
+    """solve_host() with the compact output layout (uint16 order, batch-end bit mask): fewer bytes back over
+    PCIe; unpack_compact() gives the solve_host() arrays."""
+    import torch
+    n, K = _check_inputs(I, p, g, alpha, coeffs, "host")
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    P = make_params(dict(params, K=K), stream=stream, precision=precision, algo=algo)
+    o = out if out is not None else alloc_out_compact(torch, n, K, want_w)
+    sdedge_solve_batch_host_compact(I, p, g, alpha, coeffs, n, P, o["lat"], o["gamma"], o["M"], o["batch_end_mask"],
+                                    o["order"], o["w"], o["status"])
     return o
 
 

@@ -3422,8 +3422,21 @@ struct HostPipe {
     }
 };
 
+// Compact re-encoding of a chunk's schedule for the device->host copy (sdedge_solve_batch_host_compact):
+// order as uint16, batch ends as a bit mask (zeroed by the caller).  Grid-stride over n*K elements.
+__global__ void pack_kernel(const int32_t* bend, const int32_t* order, long long n, int K, uint16_t* order16,
+                            uint32_t* mask)
+{
+    const int W = (K + 31) / 32;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n * K; i += (long long)gridDim.x * blockDim.x) {
+        order16[i] = (uint16_t)order[i];
+        const int e = bend[i];
+        if (e > 0) atomicOr(mask + (i / K) * W + (e - 1) / 32, 1u << ((e - 1) & 31));
+    }
+}
+
 int host_pipeline(HostPipe& hp, const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
-                  sdedge_schedule* o, cudaStream_t st)
+                  sdedge_schedule* o, cudaStream_t st, const sdedge_compact_schedule* oc = nullptr)
 {
     const size_t K = (size_t)p->K, nn = (size_t)n;
     const size_t bI = nn * K * 4, bD = nn * K * 8, bA = nn * 8, bC = s->coeffs ? nn * 32 : 0;
@@ -3433,6 +3446,8 @@ int host_pipeline(HostPipe& hp, const sdedge_scenarios* s, int64_t n, const sded
     const size_t oI = take(bI), oP = take(bD), oG = take(bD), oA = take(bA), oC = take(bC);
     const size_t oLat = take(bLat), oGm = take(bS), oM = take(bS), oBe = take(bI), oOr = take(bI),
                  oW = take(bW), oSt = take(bS);
+    const size_t Wm = (K + 31) / 32;
+    const size_t oMask = oc ? take(nn * Wm * 4) : 0, oO16 = oc ? take(nn * K * 2) : 0;
     int dev = 0;
     CU(cudaGetDevice(&dev));
     if (int rc2 = ws_alloc(reinterpret_cast<void**>(&hp.d), off, st)) return rc2;
@@ -3480,10 +3495,28 @@ int host_pipeline(HostPipe& hp, const sdedge_scenarios* s, int64_t n, const sded
         pc.stream = q;
         if (int rc = solve_device(&ds, m, &pc, reinterpret_cast<double*>(d + oLat) + 3 * a, &dsch)) return rc;
         launches += g_launches;
+        if (oc) {                            // re-encode on the device, copy the compact arrays back
+            CU(cudaMemsetAsync(d + oMask + Wm * 4 * a, 0, Wm * 4 * m, q));
+            const long long blocks = std::min<long long>((m * (long long)K + 255) / 256, 148LL * 16);
+            pack_kernel<<<(unsigned)blocks, 256, 0, q>>>(dsch.batch_end, dsch.order, m, (int)K,
+                                                          reinterpret_cast<uint16_t*>(d + oO16) + a * K,
+                                                          reinterpret_cast<uint32_t*>(d + oMask) + a * Wm);
+            CU(cudaGetLastError());
+            launches += 1;
+        }
         CU(cudaEventRecord(hp.evc[c], q));
         q = hp.ss[3];
         CU(cudaStreamWaitEvent(q, hp.evc[c], 0));
         CU(d2h(out_latency, oLat, 24, a, m, q));
+        if (oc) {
+            CU(d2h(oc->gamma, oGm, 4, a, m, q));
+            CU(d2h(oc->num_batches, oM, 4, a, m, q));
+            CU(d2h(oc->batch_end_mask, oMask, Wm * 4, a, m, q));
+            CU(d2h(oc->order, oO16, K * 2, a, m, q));
+            if (bW) CU(d2h(oc->bw_share, oW, K * 8, a, m, q));
+            CU(d2h(oc->status, oSt, 4, a, m, q));
+            continue;
+        }
         CU(d2h(o->gamma, oGm, 4, a, m, q));
         CU(d2h(o->num_batches, oM, 4, a, m, q));
         CU(d2h(o->batch_end, oBe, K * 4, a, m, q));
@@ -3547,6 +3580,28 @@ int sdedge_solve_batch_host(const sdedge_scenarios* s, int64_t n, const sdedge_p
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
     HostPipe hp;
     rc = host_pipeline(hp, s, n, p, out_latency, o, st);
+    const int rc2 = hp.finish(st);
+    return rc ? rc : rc2;
+}
+
+int sdedge_solve_batch_host_compact(const sdedge_scenarios* s, int64_t n, const sdedge_params* p, double* out_latency,
+                                    sdedge_compact_schedule* oc)
+{
+    // sdedge_solve_batch_host with the schedule re-encoded on the device before the copy back
+    // (pack_kernel); same chunked pipeline, same cleanup on every path
+    g_err[0] = 0;
+    g_launches = 0;
+    if (!oc) return fail(-1, "null argument");
+    if (!oc->gamma || !oc->num_batches || !oc->batch_end_mask || !oc->order || !oc->status)
+        return fail(-1, "null argument");
+    sdedge_schedule full{oc->gamma, oc->num_batches, reinterpret_cast<int32_t*>(oc->batch_end_mask),
+                         reinterpret_cast<int32_t*>(oc->order), oc->bw_share, oc->status, nullptr, nullptr, nullptr};
+    int rc = validate(s, n, p, out_latency, &full);   // (the layout pointers only need to be non-null here)
+    if (rc) return rc;
+    if (n == 0) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    HostPipe hp;
+    rc = host_pipeline(hp, s, n, p, out_latency, &full, st, oc);
     const int rc2 = hp.finish(st);
     return rc ? rc : rc2;
 }

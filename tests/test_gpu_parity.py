@@ -279,6 +279,22 @@ def test_wide_snr_range_bandwidth():
         assert gg["status"][s] == o["status"][s]
 
 
+@pytest.mark.parametrize("cfg,n", [("C3", 70000), ("C5256", 300)])
+def test_host_compact_layout(cfg, n):
+    """sdedge_solve_batch_host_compact returns exactly sdedge_solve_batch_host's results (uint16 order,
+    batch ends as a bit mask; several pipeline chunks at C3 70000, a 256-bit mask per scenario at K = 256)."""
+    import paper_2510_11331_b200 as sd
+    pd, sc, _ = scengen.config(cfg, 0, n)
+    host = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).pin_memory() for k in ("I", "p", "g", "alpha")}
+    full = sd.solve_host(pd, host["I"], host["p"], host["g"], host["alpha"])
+    comp = sd.solve_host_compact(pd, host["I"], host["p"], host["g"], host["alpha"])
+    torch.cuda.synchronize()
+    u = sd.unpack_compact(comp)
+    for k in ("lat", "gamma", "M", "batch_end", "order", "w", "status"):
+        a, b = full[k].numpy(), u[k]
+        assert np.array_equal(a, b, equal_nan=True), k
+
+
 def test_streams_and_empty_call():
     import paper_2510_11331_b200 as sd
     pd, sc, _ = scengen.config("C3", 0, 500)
