@@ -174,7 +174,9 @@ int sdedge_solve_batch_host(const sdedge_scenarios* scenarios, int64_t n, const 
  *   order          [n * K] uint16 (K <= SDEDGE_MAX_K < 2^16): original task index per sorted position;
  *   gamma, num_batches, status [n] int32 and bw_share [n * K] fp64 (or NULL) as in sdedge_schedule.
  * Host pointers (pinned memory recommended), asynchronous on params->stream like the host entry;
- * return codes and per-scenario status as sdedge_solve_batch. */
+ * return codes and per-scenario status as sdedge_solve_batch.  The outputs are the solve's own (Algorithm 1's
+ * backtracked batches; gamma*; w*, eq:opt_w P:596-612), re-encoded only.
+ * The caller owns every buffer; on failure the caller's stream still covers every copy already queued. */
 typedef struct {
     int32_t*  gamma;             /* [n]                                   */
     int32_t*  num_batches;       /* [n]                                   */
